@@ -1,0 +1,211 @@
+/*
+ * cjm.h -- C ABI of the B200-native Chebyshev-Jacobi (CJM) solver, the hot
+ * path of arXiv 1705.00103 ("Speeding up a few orders of magnitude the Jacobi
+ * method: high order Chebyshev-Jacobi over GPUs").
+ *
+ * Citation keys: P:L = PAPER.md line L (section / equation named beside it);
+ * S:L = SPEC.md line L; DESIGN R# = reading
+ *
+ * The method (section 2.1): a weighted classical Jacobi iteration
+ *     u_{n+1} = u_n + w_n D^{-1} (b - A u_n)
+ * with a different weight w_n at every sweep, the weights being "a
+ * transformation of the zeros of a Chebyshev polynomial" that depends on "the
+ * resolution of the mesh, the boundary conditions and the required
+ * tolerance", applied cyclically until "reaching a prescribed
+ * tolerance".  A = Delta_h is the 5-point (tab:ste2),
+ * 9-point alpha=2/3 (Eq. 9-points) or 17-point alpha=2/3
+ * (Eq. 17-points) Laplacian on a uniform grid with
+ * Dirichlet data.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - nx, ny: interior unknowns (DESIGN R1: the paper's N_x = nx+1 intervals).
+ *    Node (i,j), 1 <= i <= nx, 1 <= j <= ny, sits at (i h, j h).
+ *  - r = stencil reach: 1 for the 5- and 9-point, 2 for the 17-point
+ *    (the paper's 3x3 and 5x5 masks, tab:ste1 / P:403-409).
+ *  - u: fp64, row-major, WITH its r ghost rings: (rows_u) x (nx + 2r) values
+ *    in rows of pitch ld_u >= nx + 2r doubles; node (i,j) at
+ *    u[(j - 1 + r) * ld_u + (i - 1 + r)].  Ghost values are the Dirichlet
+ *    data and are never written.  Interior values are the initial guess on
+ *    entry and the solution on return.
+ *  - rhs: fp64, row-major, interior only: ny x nx values of pitch
+ *    ld_rhs >= nx; node (i,j) at rhs[(j-1) * ld_rhs + (i-1)].  rhs is b in
+ *    PDE units (Delta u = b, the paper's test problem P:441); read only.
+ *  - Multi-GPU (world_size > 1): rank g owns the row slab
+ *    [y0, y0 + ny_local) of the global interior rows (cjm_plan_info); u and
+ *    rhs are then the LOCAL slab (rows_u = ny_local + 2r, rhs ny_local rows).
+ *    Ghost rows that border another rank are filled by the library (halo
+ *    exchange); only ranks 0 and world_size-1 need real top / bottom data.
+ *  - Every call returns a cjm_status; no exception crosses the ABI.  On
+ *    CJM_ERR_CUDA / CJM_ERR_NCCL, cjm_last_error() gives the message.
+ *  - Thread compatibility: a plan may be used by one host thread at a time.
+ *  - Device pointers must come from cudaMalloc-class allocations on the
+ *    plan's device (e.g. torch CUDA tensors); host pointers may be pageable
+ *    or pinned (pinned is faster).
+ */
+#ifndef CJM_H
+#define CJM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CJM_VERSION_MAJOR 0
+#define CJM_VERSION_MINOR 1
+
+typedef enum {
+    CJM_OK = 0,
+    CJM_ERR_INVALID_ARG = 1,   /* bad size / pointer / tol / option */
+    CJM_ERR_UNSUPPORTED = 2,   /* e.g. a boundary condition other than Dirichlet */
+    CJM_ERR_NOT_CONVERGED = 3, /* max_cycles reached */
+    CJM_ERR_DIVERGED = 4,      /* non-finite residual */
+    CJM_ERR_STAGNATED = 5,     /* a cycle reduced ||r||_2 by less than 2x (fp64 floor) */
+    CJM_ERR_CUDA = 6,
+    CJM_ERR_NCCL = 7,
+    CJM_ERR_OOM = 8
+} cjm_status;
+
+/* The three Laplacians of the paper (value = number of points). */
+typedef enum { CJM_STENCIL_5 = 5, CJM_STENCIL_9 = 9, CJM_STENCIL_17 = 17 } cjm_stencil;
+
+/* Only Dirichlet data is covered by the paper's closed-form kappa bounds
+ * (S:322).  Any other value -> CJM_ERR_UNSUPPORTED. */
+typedef enum { CJM_BC_DIRICHLET = 0 } cjm_bc;
+
+/* Order in which the weights of a cycle are applied (DESIGN R3; the paper is
+ * silent).  LEBEDEV23 is the stable default; ASCENDING is SPEC's order
+ * (S:309), unstable in fp64, offered for tests only. */
+typedef enum { CJM_ORDER_LEBEDEV23 = 0, CJM_ORDER_ASCENDING = 1 } cjm_order;
+
+/* CHEBYSHEV = the CJM.  JACOBI = the classical Jacobi baseline the
+ * paper compares against (w = 1); its "cycle" is a
+ * check interval of jacobi_check sweeps and it has no stagnation test. */
+typedef enum { CJM_METHOD_CHEBYSHEV = 0, CJM_METHOD_JACOBI = 1 } cjm_method;
+
+typedef struct {
+    int max_cycles;        /* default 8 (Jacobi: default 100000) */
+    int order;             /* cjm_order, default CJM_ORDER_LEBEDEV23 */
+    int method;            /* cjm_method, default CJM_METHOD_CHEBYSHEV */
+    int jacobi_check;      /* Jacobi check interval in sweeps, default 1024 */
+    int world_size;        /* default 1 (single GPU) */
+    int rank;              /* default 0 */
+    const void *nccl_id;   /* 128-byte ncclUniqueId from cjm_get_nccl_id on rank 0,
+                              broadcast by the caller; required when world_size > 1 */
+    int device;            /* CUDA device ordinal; -1 (default) = current device */
+    /* tuning knobs, 0 = automatic */
+    int tile_w;            /* columns per CTA strip: 128 or 256 */
+    int ctas_per_sm;       /* resident CTAs per SM of the persistent sweep grid */
+    int stages;            /* depth of the TMA row ring */
+    int graph_chunk;       /* sweeps captured per CUDA graph */
+} cjm_options;
+
+typedef struct {
+    long long iterations;  /* sweeps applied to the returned iterate */
+    int cycles;            /* completed cycles (checks after r0) */
+    int status;            /* cjm_status of the solve */
+    long long cycle_len;   /* P (sweeps per cycle) */
+    long long m_min;       /* minimal Chebyshev degree M for tol */
+    double kappa_min, kappa_max;
+    double r0_l2, r0_linf; /* ||b - Delta_h u_0||, PDE units, global */
+    double r_l2, r_linf;   /* same for the returned iterate */
+    double plan_s;         /* host seconds spent in cjm_plan */
+    double solve_s;        /* device seconds of the solve (CUDA events, whole call) */
+    double sweep_s;        /* device seconds of the non-check sweeps (CUDA events) */
+    long long sweeps_timed;/* number of sweeps inside sweep_s */
+    long long kernel_launches; /* kernels of this library launched by the call */
+    double h2d_bytes, d2h_bytes;  /* host<->device bytes moved by the call */
+} cjm_report;
+
+typedef struct cjm_plan_s *cjm_plan_t;
+
+/* Fill *opt with the defaults above. */
+void cjm_default_options(cjm_options *opt);
+
+/* Host-only scheduler (no GPU needed): SURVEY section 8(a) rows a1-a4.
+ *   kappa bounds (5-pt classical S:252) at
+ *   N_x = nx+1, N_y = ny+1 (DESIGN R1); M_min = ceil(acosh(1/tol)/acosh(mu))
+ *   (DESIGN R5); P = smallest 2^a 3^b >= M_min and the application
+ *   order t_1..t_P (DESIGN R3); w_k = 1/(kmin + (kmax-kmin) sin^2(t_k pi/4P)).
+ * Outputs: kappa_min, kappa_max, m_min, cycle_len (= P) always (nullable);
+ * t_out / w_out (nullable) receive P entries if capacity >= P, else
+ * CJM_ERR_INVALID_ARG (call once with capacity 0 to learn P).
+ * Errors: INVALID_ARG for nx or ny < 4, tol outside (0,1), an
+ * unknown stencil or order. */
+cjm_status cjm_schedule(int stencil, int nx, int ny, double tol, int order,
+                        double *kappa_min, double *kappa_max,
+                        long long *m_min, long long *cycle_len,
+                        long long *t_out, double *w_out, long long capacity);
+
+/* Build a plan: run the scheduler, pick the launch configuration, allocate
+ * the work buffers on the device (two iterate buffers, g = D^-1 b, the
+ * weights, reduction scratch, the NCCL communicator when world_size > 1)
+ * and copy the weights host->device once.
+ *   h: uniform mesh spacing, > 0 and finite.
+ * Ownership: the plan owns all its buffers until cjm_plan_destroy.
+ * Errors: INVALID_ARG (sizes, h, tol, options; a slab thinner than 2r+1
+ * rows), UNSUPPORTED (bc), OOM, CUDA, NCCL.  *out is NULL on error. */
+cjm_status cjm_plan(cjm_plan_t *out, int stencil, int nx, int ny, double h,
+                    int bc, double tol, const cjm_options *opt);
+
+/* Static facts of a plan.  Any output pointer may be NULL.
+ *   info: kappa_min/max, m_min, cycle_len (other fields zero) and plan_s.
+ *   reach: r.  y0 / ny_local: this rank's slab of interior rows (0-based).
+ *   host_weights: the P weights in application order (owned by the plan). */
+cjm_status cjm_plan_info(cjm_plan_t p, cjm_report *info, int *reach,
+                         int *y0, int *ny_local, const double **host_weights);
+
+/* Solve on the device (P:298-309 with the data already resident).
+ *   rhs (device, ny_local x nx, pitch ld_rhs), u (device, (ny_local+2r) x
+ *   (nx+2r), pitch ld_u): see the conventions above.  All work is enqueued
+ *   on `cuda_stream` (a cudaStream_t; NULL = legacy default stream) and the
+ *   call synchronises that stream once per cycle to read the residual
+ *   (SURVEY section 3).  On return the interior of u holds the iterate after
+ *   rep->iterations sweeps: for CJM_OK the first cycle-boundary iterate with
+ *   ||r||_2 <= tol ||r_0||_2 (DESIGN R4); for NOT_CONVERGED / STAGNATED /
+ *   DIVERGED the last cycle-boundary iterate.  rep (nullable) is filled in
+ *   every case.  Multi-GPU: collective, every rank calls it. */
+cjm_status cjm_solve(cjm_plan_t p, const double *rhs, long long ld_rhs,
+                     double *u, long long ld_u, void *cuda_stream,
+                     cjm_report *rep);
+
+/* The same solve with HOST buffers: one host->device copy of u and rhs at
+ * the start and one device->host copy of the solution at the end (the
+ * paper's flow), all inside the call.  Layouts as cjm_solve. */
+cjm_status cjm_solve_host(cjm_plan_t p, const double *rhs_host, long long ld_rhs,
+                          double *u_host, long long ld_u, void *cuda_stream,
+                          cjm_report *rep);
+
+/* Apply `count` scheduled sweeps with no stop test: sweep k (0 <= k < count)
+ * uses the weight at cycle position (first + k) mod P.  u (device) is read
+ * and overwritten with the result (interior only).  Used to compare a fixed
+ * segment of the iteration with the oracle at any size.  rep (nullable)
+ * receives sweep_s / sweeps_timed / kernel_launches. */
+cjm_status cjm_sweeps(cjm_plan_t p, const double *rhs, long long ld_rhs,
+                      double *u, long long ld_u, long long first, long long count,
+                      void *cuda_stream, cjm_report *rep);
+
+/* Residual norms of u: ||b - Delta_h u||_2 and ||.||_inf over the (global)
+ * interior, in PDE units (fused reduction kernel, allreduced across ranks).
+ * Synchronises cuda_stream.  l2 / linf nullable. */
+cjm_status cjm_residual(cjm_plan_t p, const double *rhs, long long ld_rhs,
+                        const double *u, long long ld_u, void *cuda_stream,
+                        double *l2, double *linf);
+
+/* Create an NCCL unique id (128 bytes) for a multi-GPU plan (rank 0). */
+cjm_status cjm_get_nccl_id(void *out128);
+
+/* Slab geometry of the 1-D row decomposition (host only): rank g of
+ * world_size owns interior rows [floor(g ny / W), floor((g+1) ny / W)). */
+cjm_status cjm_slab(int ny, int world_size, int rank, int *y0, int *ny_local);
+
+/* Free every device buffer, graph and communicator of the plan. NULL is ok. */
+cjm_status cjm_plan_destroy(cjm_plan_t p);
+
+const char *cjm_status_str(int status);
+const char *cjm_last_error(void);
+int cjm_version(void);   /* 100 * major + minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CJM_H */

@@ -81,6 +81,8 @@ def lib():
                                       dp, C.c_long, dp, dp]
         L.oracle_solve.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                                    dp, C.c_long, dp, C.c_long, dp, C.c_long, C.POINTER(Report)]
+        L.oracle_sweeps.argtypes = [C.c_int, C.c_int, C.c_int, dp, C.c_long, dp, C.c_long, dp,
+                                    C.c_long, C.c_long, C.c_long]
         L.oracle_num_threads.restype = C.c_int
         L.oracle_set_num_threads.argtypes = [C.c_int]
         _lib = L
@@ -158,6 +160,19 @@ def sweep(stencil: int, u: np.ndarray, g: np.ndarray, w: float) -> np.ndarray:
     assert g.shape == (ny, nx)
     out = u.copy()
     lib().oracle_sweep(stencil, nx, ny, _dp(u), u.shape[1], _dp(g), nx, w, _dp(out), u.shape[1])
+    return out
+
+
+def sweeps(stencil: int, u: np.ndarray, g: np.ndarray, w: np.ndarray, first: int,
+           count: int) -> np.ndarray:
+    """`count` scheduled sweeps (weight w[(first+k) mod P] at sweep k)."""
+    r = reach(stencil)
+    out = np.array(u, dtype=np.float64, order="C", copy=True)
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    ny, nx = out.shape[0] - 2 * r, out.shape[1] - 2 * r
+    lib().oracle_sweeps(stencil, nx, ny, _dp(out), out.shape[1], _dp(g), nx, _dp(w), len(w),
+                        first, count)
     return out
 
 

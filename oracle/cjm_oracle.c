@@ -325,6 +325,30 @@ void oracle_residual(int stencil, int nx, int ny, double h,
     free(g);
 }
 
+/* `count` consecutive sweeps of the schedule (weight w[(first + k) mod P] at
+ * sweep k), double buffered exactly as in oracle_solve; u is overwritten with
+ * the result.  Used for fixed segments of a solve at sizes where the whole
+ * solve would take the oracle too long. */
+int oracle_sweeps(int stencil, int nx, int ny, double *u, long ldu,
+                  const double *g, long ldg, const double *w, long P,
+                  long first, long count)
+{
+    int r = oracle_reach(stencil);
+    long rows = ny + 2 * r;
+    double *v = (double *)malloc(sizeof(double) * (size_t)rows * ldu);
+    if (!v) return OR_OOM;
+    memcpy(v, u, sizeof(double) * (size_t)rows * ldu);
+    double *cur = u, *nxt = v;
+    for (long k = 0; k < count; k++) {
+        oracle_sweep(stencil, nx, ny, cur, ldu, g, ldg, w[(first + k) % P], nxt, ldu);
+        double *tmp = cur; cur = nxt; nxt = tmp;
+    }
+    if (cur != u)
+        memcpy(u, cur, sizeof(double) * (size_t)rows * ldu);
+    free(v);
+    return OR_OK;
+}
+
 typedef struct {
     long long iterations;
     int cycles;

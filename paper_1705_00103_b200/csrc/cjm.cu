@@ -1,0 +1,683 @@
+// libcjm: plan, executor and C ABI of the B200-native CJM (include/cjm.h).
+//
+// Executor (SURVEY section 3 "New build"):
+//   setup (row a5)      : u -> both iterate buffers (cudaMemcpy2DAsync into the
+//                         pitched, 32-byte aligned internal layout), rhs -> g,
+//                         g *= h^2/c_C (cjm_scale_kernel), n = 0
+//   sweep 0 + reduction : ||r_0|| (check kernel, one 16-byte D2H, one sync)
+//   hot loop            : sweeps 1..P-1 of each cycle replayed from CUDA graphs
+//                         of identical sweep launches (each kernel reads n)
+//   check sweep n = cP  : fused reduction of u_{cP}, one D2H + sync per cycle,
+//                         host stop decision (row a8, DESIGN R4)
+//   multi-GPU           : NCCL halo exchange of r rows after every sweep (a9)
+//                         and sum/max allreduce of the reduction (a10)
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+
+#include "../../include/cjm.h"
+#include "internal.h"
+#include "sweep.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void set_error(const char* what, const char* msg) {
+  g_last_error = std::string(what) + ": " + msg;
+}
+
+#define CUDA_TRY(expr)                                            \
+  do {                                                            \
+    cudaError_t e_ = (expr);                                      \
+    if (e_ != cudaSuccess) {                                      \
+      set_error(#expr, cudaGetErrorString(e_));                   \
+      return e_ == cudaErrorMemoryAllocation ? CJM_ERR_OOM : CJM_ERR_CUDA; \
+    }                                                             \
+  } while (0)
+
+#define NCCL_TRY(expr)                                            \
+  do {                                                            \
+    ncclResult_t r_ = (expr);                                     \
+    if (r_ != ncclSuccess) {                                      \
+      set_error(#expr, ncclGetErrorString(r_));                   \
+      return CJM_ERR_NCCL;                                        \
+    }                                                             \
+  } while (0)
+
+#define STATUS_TRY(expr)                  \
+  do {                                    \
+    cjm_status s_ = (expr);               \
+    if (s_ != CJM_OK) return s_;          \
+  } while (0)
+
+enum Mode { MODE_HOT = 0, MODE_CHECK = 1, MODE_RESID = 2 };
+
+using KernelFn = void (*)(const cjm::SweepParams);
+
+template <int ST, int W>
+KernelFn pick_mode(int mode) {
+  switch (mode) {
+    case MODE_HOT: return cjm::cjm_sweep_kernel<ST, W, false, true>;
+    case MODE_CHECK: return cjm::cjm_sweep_kernel<ST, W, true, true>;
+    default: return cjm::cjm_sweep_kernel<ST, W, true, false>;
+  }
+}
+
+template <int ST>
+KernelFn pick_w(int W, int mode) {
+  return W == 128 ? pick_mode<ST, 128>(mode) : pick_mode<ST, 256>(mode);
+}
+
+KernelFn pick_kernel(int stencil, int W, int mode) {
+  switch (stencil) {
+    case 5: return pick_w<5>(W, mode);
+    case 9: return pick_w<9>(W, mode);
+    default: return pick_w<17>(W, mode);
+  }
+}
+
+__global__ void set_counter_kernel(unsigned long long* ctr, unsigned long long v) { *ctr = v; }
+
+}  // namespace
+
+struct cjm_plan_s {
+  // problem
+  int stencil = 9, R = 1, nx = 0, ny = 0, y0 = 0, ny_local = 0;
+  double h = 0, tol = 0, gscale = 0;
+  int method = CJM_METHOD_CHEBYSHEV, max_cycles = 8;
+  cjm::Schedule sched;
+  long long P = 0;
+  // distribution
+  int world = 1, rank = 0, device = 0;
+  ncclComm_t comm = nullptr;
+  // device memory
+  long long ld = 0;
+  size_t buf_elems = 0, g_elems = 0;
+  double* buf[2] = {nullptr, nullptr};
+  double* G = nullptr;
+  double* w_dev = nullptr;
+  double* partials = nullptr;
+  double* result = nullptr;
+  double* result_host = nullptr;  // pinned, 2 doubles
+  unsigned long long* ctr = nullptr;
+  unsigned int* ticket = nullptr;
+  // launch configuration
+  int W = 256, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 256;
+  size_t smem = 0;
+  cudaStream_t cap_stream = nullptr;
+  std::map<std::pair<long long, int>, cudaGraphExec_t> graphs;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double plan_s = 0;
+};
+
+namespace {
+
+cjm_status launch_sweep(cjm_plan_s* pl, int mode, cudaStream_t st) {
+  cjm::SweepParams sp;
+  sp.buf0 = pl->buf[0];
+  sp.buf1 = pl->buf[1];
+  sp.g = pl->G;
+  sp.w = pl->w_dev;
+  sp.ctr = pl->ctr;
+  sp.ticket = pl->ticket;
+  sp.partials = pl->partials;
+  sp.result = pl->result;
+  sp.P = pl->P;
+  sp.ld = pl->ld;
+  sp.nx = pl->nx;
+  sp.rows = pl->ny_local;
+  sp.row0 = 0;
+  sp.stages = pl->stages;
+  sp.advance = 1;
+  const long long nstrips = (pl->nx + pl->W - 1) / pl->W;
+  sp.units = nstrips * pl->ny_local;
+  KernelFn k = pick_kernel(pl->stencil, pl->W, mode);
+  k<<<pl->nctas, pl->W + 32, pl->smem, st>>>(sp);
+  CUDA_TRY(cudaGetLastError());
+  return CJM_OK;
+}
+
+// Halo exchange of the iterate buffer `b` (row a9): my first / last R interior
+// rows to the neighbours' ghost rows.  Rows are contiguous R*ld doubles.
+cjm_status halo_exchange(cjm_plan_s* pl, double* b, cudaStream_t st) {
+  if (pl->world == 1) return CJM_OK;
+  const size_t cnt = (size_t)pl->R * pl->ld;
+  double* first_rows = b + (long long)pl->R * pl->ld;          // interior rows 0..R-1
+  double* last_rows = b + (long long)pl->ny_local * pl->ld;     // interior rows ny-R..ny-1
+  double* ghost_lo = b;                                           // ghost rows -R..-1
+  double* ghost_hi = b + (long long)(pl->ny_local + pl->R) * pl->ld;
+  NCCL_TRY(ncclGroupStart());
+  if (pl->rank > 0) {
+    NCCL_TRY(ncclSend(first_rows, cnt, ncclDouble, pl->rank - 1, pl->comm, st));
+    NCCL_TRY(ncclRecv(ghost_lo, cnt, ncclDouble, pl->rank - 1, pl->comm, st));
+  }
+  if (pl->rank < pl->world - 1) {
+    NCCL_TRY(ncclSend(last_rows, cnt, ncclDouble, pl->rank + 1, pl->comm, st));
+    NCCL_TRY(ncclRecv(ghost_hi, cnt, ncclDouble, pl->rank + 1, pl->comm, st));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return CJM_OK;
+}
+
+// One hot sweep reading buffer parity `par` (= n & 1) then the halo exchange
+// of its output.
+cjm_status hot_sweep(cjm_plan_s* pl, int par, cudaStream_t st) {
+  STATUS_TRY(launch_sweep(pl, MODE_HOT, st));
+  return halo_exchange(pl, pl->buf[par ^ 1], st);
+}
+
+cjm_status get_graph(cjm_plan_s* pl, long long len, int par, cudaGraphExec_t* out) {
+  const int key_par = pl->world > 1 ? par : 0;   // single GPU: buffers resolved on device
+  auto it = pl->graphs.find({len, key_par});
+  if (it != pl->graphs.end()) { *out = it->second; return CJM_OK; }
+  cudaGraph_t graph = nullptr;
+  CUDA_TRY(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
+  cjm_status s = CJM_OK;
+  for (long long k = 0; k < len && s == CJM_OK; ++k) s = hot_sweep(pl, (int)((par + k) & 1), pl->cap_stream);
+  cudaError_t e = cudaStreamEndCapture(pl->cap_stream, &graph);
+  if (s != CJM_OK) { if (graph) cudaGraphDestroy(graph); return s; }
+  CUDA_TRY(e);
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CUDA_TRY(e);
+  pl->graphs[{len, key_par}] = exec;
+  *out = exec;
+  return CJM_OK;
+}
+
+// Run `count` hot sweeps starting at global sweep index n0 (host-tracked).
+cjm_status run_hot(cjm_plan_s* pl, long long n0, long long count, cudaStream_t st,
+                   long long* launches) {
+  long long done = 0;
+  while (done < count) {
+    const long long len = std::min<long long>(pl->graph_chunk, count - done);
+    cudaGraphExec_t ex;
+    STATUS_TRY(get_graph(pl, len, (int)((n0 + done) & 1), &ex));
+    CUDA_TRY(cudaGraphLaunch(ex, st));
+    done += len;
+    *launches += len;
+  }
+  return CJM_OK;
+}
+
+// Check sweep (fused reduction) + global sum/max + D2H of the two scalars.
+cjm_status check_sweep(cjm_plan_s* pl, int mode, long long n, cudaStream_t st, double* s, double* m,
+                       long long* launches) {
+  STATUS_TRY(launch_sweep(pl, mode, st));
+  *launches += 1;
+  if (mode == MODE_CHECK) STATUS_TRY(halo_exchange(pl, pl->buf[(n & 1) ^ 1], st));
+  if (pl->world > 1) {
+    NCCL_TRY(ncclGroupStart());
+    NCCL_TRY(ncclAllReduce(pl->result, pl->result, 1, ncclDouble, ncclSum, pl->comm, st));
+    NCCL_TRY(ncclAllReduce(pl->result + 1, pl->result + 1, 1, ncclDouble, ncclMax, pl->comm, st));
+    NCCL_TRY(ncclGroupEnd());
+  }
+  CUDA_TRY(cudaMemcpyAsync(pl->result_host, pl->result, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *s = pl->result_host[0];
+  *m = pl->result_host[1];
+  return CJM_OK;
+}
+
+cjm_status set_counter(cjm_plan_s* pl, unsigned long long v, cudaStream_t st) {
+  set_counter_kernel<<<1, 1, 0, st>>>(pl->ctr, v);
+  CUDA_TRY(cudaGetLastError());
+  return CJM_OK;
+}
+
+// Row a5: user layout -> internal buffers.  kind = H2D or D2D.
+cjm_status stage_in(cjm_plan_s* pl, const double* rhs, long long ld_rhs, const double* u,
+                    long long ld_u, bool both, cudaMemcpyKind kind, cudaStream_t st) {
+  const int R = pl->R;
+  const size_t upitch = (size_t)pl->ld * sizeof(double);
+  CUDA_TRY(cudaMemcpy2DAsync(pl->buf[0] + (cjm::PADL - R), upitch, u, (size_t)ld_u * sizeof(double),
+                             (size_t)(pl->nx + 2 * R) * sizeof(double), (size_t)(pl->ny_local + 2 * R),
+                             kind, st));
+  if (both)
+    CUDA_TRY(cudaMemcpyAsync(pl->buf[1], pl->buf[0], pl->buf_elems * sizeof(double),
+                             cudaMemcpyDeviceToDevice, st));
+  if (rhs) {
+    CUDA_TRY(cudaMemcpy2DAsync(pl->G + cjm::PADL, upitch, rhs, (size_t)ld_rhs * sizeof(double),
+                               (size_t)pl->nx * sizeof(double), (size_t)pl->ny_local, kind, st));
+    const long long total = (long long)pl->nx * pl->ny_local;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    cjm::cjm_scale_kernel<<<blocks, 256, 0, st>>>(pl->G, pl->ld, pl->nx, pl->ny_local, pl->gscale);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return CJM_OK;
+}
+
+cjm_status stage_out(cjm_plan_s* pl, int which, double* u, long long ld_u, cudaMemcpyKind kind,
+                     cudaStream_t st) {
+  const int R = pl->R;
+  CUDA_TRY(cudaMemcpy2DAsync(u + (long long)R * ld_u + R, (size_t)ld_u * sizeof(double),
+                             pl->buf[which] + (long long)R * pl->ld + cjm::PADL,
+                             (size_t)pl->ld * sizeof(double), (size_t)pl->nx * sizeof(double),
+                             (size_t)pl->ny_local, kind, st));
+  return CJM_OK;
+}
+
+bool check_layout(const cjm_plan_s* pl, const void* rhs, long long ld_rhs, const void* u,
+                  long long ld_u) {
+  return pl && u && ld_u >= pl->nx + 2 * pl->R && (!rhs || ld_rhs >= pl->nx);
+}
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms * 1e-3;
+}
+
+void fill_static(const cjm_plan_s* pl, cjm_report* r) {
+  std::memset(r, 0, sizeof(*r));
+  r->cycle_len = pl->P;
+  r->m_min = pl->sched.m_min;
+  r->kappa_min = pl->sched.kmin;
+  r->kappa_max = pl->sched.kmax;
+  r->plan_s = pl->plan_s;
+}
+
+// The whole solve (rows a5-a10); `kind` selects device or host user buffers.
+cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, double* u,
+                      long long ld_u, cudaMemcpyKind kin, cudaMemcpyKind kout, void* stream,
+                      cjm_report* rep_out) {
+  if (!check_layout(pl, rhs, ld_rhs, u, ld_u) || !rhs) {
+    set_error("cjm_solve", "invalid pointer or pitch");
+    return CJM_ERR_INVALID_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(pl->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  cjm_report rep;
+  fill_static(pl, &rep);
+  const double sc = std::fabs(pl->gscale);
+  long long launches = 0;
+
+  CUDA_TRY(cudaEventRecord(pl->ev[0], st));
+  STATUS_TRY(stage_in(pl, rhs, ld_rhs, u, ld_u, true, kin, st));
+  launches += 1;
+  if (kin == cudaMemcpyHostToDevice) {
+    rep.h2d_bytes = (double)(pl->ny_local + 2 * pl->R) * (pl->nx + 2 * pl->R) * 8.0 +
+                    (double)pl->ny_local * pl->nx * 8.0;
+  }
+  STATUS_TRY(set_counter(pl, 0ull, st));
+  launches += 1;
+  STATUS_TRY(halo_exchange(pl, pl->buf[0], st));
+
+  double s, m;
+  STATUS_TRY(check_sweep(pl, MODE_CHECK, 0, st, &s, &m, &launches));
+  rep.r0_l2 = std::sqrt(s) / sc;
+  rep.r0_linf = m / sc;
+  rep.r_l2 = rep.r0_l2;
+  rep.r_linf = rep.r0_linf;
+
+  int status = CJM_ERR_NOT_CONVERGED;
+  long long n_out = 0;   // sweep index of the exported iterate
+  if (rep.r0_l2 == 0.0) {
+    status = CJM_OK;
+  } else if (!std::isfinite(rep.r0_l2)) {
+    status = CJM_ERR_DIVERGED;
+  } else {
+    double rho_prev = rep.r0_l2;
+    for (int c = 1; c <= pl->max_cycles; ++c) {
+      const long long n0 = (long long)(c - 1) * pl->P + 1;
+      CUDA_TRY(cudaEventRecord(pl->ev[2], st));
+      STATUS_TRY(run_hot(pl, n0, pl->P - 1, st, &launches));
+      CUDA_TRY(cudaEventRecord(pl->ev[3], st));
+      const long long n = (long long)c * pl->P;
+      STATUS_TRY(check_sweep(pl, MODE_CHECK, n, st, &s, &m, &launches));
+      rep.sweep_s += elapsed_s(pl->ev[2], pl->ev[3]);
+      rep.sweeps_timed += pl->P - 1;
+      const double rho = std::sqrt(s) / sc;
+      rep.cycles = c;
+      rep.iterations = n;
+      rep.r_l2 = rho;
+      rep.r_linf = m / sc;
+      n_out = n;
+      if (!std::isfinite(rho)) { status = CJM_ERR_DIVERGED; break; }
+      if (rho <= pl->tol * rep.r0_l2) { status = CJM_OK; break; }
+      if (pl->method == CJM_METHOD_CHEBYSHEV && rho > 0.5 * rho_prev) {
+        status = CJM_ERR_STAGNATED;
+        break;
+      }
+      rho_prev = rho;
+    }
+  }
+  STATUS_TRY(stage_out(pl, (int)(n_out & 1), u, ld_u, kout, st));
+  if (kout == cudaMemcpyDeviceToHost) rep.d2h_bytes = (double)pl->ny_local * pl->nx * 8.0;
+  CUDA_TRY(cudaEventRecord(pl->ev[1], st));
+  CUDA_TRY(cudaEventSynchronize(pl->ev[1]));
+  rep.solve_s = elapsed_s(pl->ev[0], pl->ev[1]);
+  rep.kernel_launches = launches;
+  rep.status = status;
+  if (rep_out) *rep_out = rep;
+  return (cjm_status)status;
+}
+
+}  // namespace
+
+// =========================================================================
+// C ABI
+// =========================================================================
+extern "C" {
+
+void cjm_default_options(cjm_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->max_cycles = 0;   // method-dependent default
+  o->order = CJM_ORDER_LEBEDEV23;
+  o->method = CJM_METHOD_CHEBYSHEV;
+  o->jacobi_check = 1024;
+  o->world_size = 1;
+  o->rank = 0;
+  o->nccl_id = nullptr;
+  o->device = -1;
+}
+
+cjm_status cjm_schedule(int stencil, int nx, int ny, double tol, int order, double* kappa_min,
+                        double* kappa_max, long long* m_min, long long* cycle_len,
+                        long long* t_out, double* w_out, long long capacity) {
+  if (!cjm::stencil_reach(stencil) || nx < 4 || ny < 4 || !(tol > 0.0 && tol < 1.0) ||
+      (order != CJM_ORDER_LEBEDEV23 && order != CJM_ORDER_ASCENDING)) {
+    set_error("cjm_schedule", "invalid argument");
+    return CJM_ERR_INVALID_ARG;
+  }
+  cjm::Schedule s;
+  if (!cjm::build_schedule(stencil, nx, ny, tol, order, &s)) return CJM_ERR_INVALID_ARG;
+  if (kappa_min) *kappa_min = s.kmin;
+  if (kappa_max) *kappa_max = s.kmax;
+  if (m_min) *m_min = s.m_min;
+  if (cycle_len) *cycle_len = s.P;
+  if (t_out || w_out) {
+    if (capacity < s.P) {
+      set_error("cjm_schedule", "capacity < cycle length");
+      return CJM_ERR_INVALID_ARG;
+    }
+    for (long long k = 0; k < s.P; ++k) {
+      if (t_out) t_out[k] = s.t[k];
+      if (w_out) w_out[k] = s.w[k];
+    }
+  }
+  return CJM_OK;
+}
+
+cjm_status cjm_slab(int ny, int world_size, int rank, int* y0, int* ny_local) {
+  if (ny < 1 || world_size < 1 || rank < 0 || rank >= world_size) return CJM_ERR_INVALID_ARG;
+  const long long a = (long long)rank * ny / world_size;
+  const long long b = (long long)(rank + 1) * ny / world_size;
+  if (y0) *y0 = (int)a;
+  if (ny_local) *ny_local = (int)(b - a);
+  return CJM_OK;
+}
+
+cjm_status cjm_get_nccl_id(void* out128) {
+  if (!out128) return CJM_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return CJM_OK;
+}
+
+cjm_status cjm_plan_destroy(cjm_plan_t p) {
+  if (!p) return CJM_OK;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+  p->graphs.clear();
+  for (auto& e : p->ev) if (e) cudaEventDestroy(e);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  cudaFree(p->buf[0]);
+  cudaFree(p->buf[1]);
+  cudaFree(p->G);
+  cudaFree(p->w_dev);
+  cudaFree(p->partials);
+  cudaFree(p->result);
+  cudaFree(p->ctr);
+  cudaFree(p->ticket);
+  if (p->result_host) cudaFreeHost(p->result_host);
+  if (p->comm) ncclCommDestroy(p->comm);
+  delete p;
+  return CJM_OK;
+}
+
+cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int bc, double tol,
+                    const cjm_options* opt_in) {
+  if (!out) return CJM_ERR_INVALID_ARG;
+  *out = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  cjm_options opt;
+  cjm_default_options(&opt);
+  if (opt_in) opt = *opt_in;
+  if (bc != CJM_BC_DIRICHLET) {
+    set_error("cjm_plan", "only Dirichlet boundary conditions are supported");
+    return CJM_ERR_UNSUPPORTED;
+  }
+  const int R = cjm::stencil_reach(stencil);
+  if (!R || nx < 4 || ny < 4 || !(h > 0.0) || !std::isfinite(h) || !(tol > 0.0 && tol < 1.0) ||
+      opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size ||
+      (opt.world_size > 1 && !opt.nccl_id) ||
+      (opt.method != CJM_METHOD_CHEBYSHEV && opt.method != CJM_METHOD_JACOBI) ||
+      (opt.tile_w != 0 && opt.tile_w != 128 && opt.tile_w != 256) || opt.stages < 0 ||
+      opt.stages > 32 || opt.ctas_per_sm < 0 || opt.graph_chunk < 0 || opt.max_cycles < 0 ||
+      opt.jacobi_check < 0) {
+    set_error("cjm_plan", "invalid argument");
+    return CJM_ERR_INVALID_ARG;
+  }
+  int y0 = 0, nyl = 0;
+  cjm_slab(ny, opt.world_size, opt.rank, &y0, &nyl);
+  if (opt.world_size > 1 && nyl < 2 * R + 1) {
+    set_error("cjm_plan", "slab thinner than 2r+1 rows");
+    return CJM_ERR_INVALID_ARG;
+  }
+
+  cjm_plan_s* pl = new cjm_plan_s;
+  pl->stencil = stencil;
+  pl->R = R;
+  pl->nx = nx;
+  pl->ny = ny;
+  pl->y0 = y0;
+  pl->ny_local = nyl;
+  pl->h = h;
+  pl->tol = tol;
+  // g = (h^2 / c_C) b, c_C = -4, -20/6, -300/72 (DESIGN R6)
+  pl->gscale = stencil == 5 ? -(h * h) * 0.25 : stencil == 9 ? -(h * h) * 0.3
+                                                             : -(h * h) * (72.0 / 300.0);
+  pl->method = opt.method;
+  pl->world = opt.world_size;
+  pl->rank = opt.rank;
+
+  if (!cjm::build_schedule(stencil, nx, ny, tol, opt.order, &pl->sched)) {
+    delete pl;
+    set_error("cjm_plan", "invalid order");
+    return CJM_ERR_INVALID_ARG;
+  }
+  if (opt.method == CJM_METHOD_JACOBI) {
+    pl->P = opt.jacobi_check > 0 ? opt.jacobi_check : 1024;
+    pl->sched.w.assign(pl->P, 1.0);
+    pl->sched.t.assign(pl->P, 0);
+    pl->max_cycles = opt.max_cycles > 0 ? opt.max_cycles : 100000;
+  } else {
+    pl->P = pl->sched.P;
+    pl->max_cycles = opt.max_cycles > 0 ? opt.max_cycles : 8;
+  }
+
+  auto fail = [&](cjm_status s) { cjm_plan_destroy(pl); return s; };
+#define PLAN_CUDA(expr)                                                  \
+  do {                                                                   \
+    cudaError_t e_ = (expr);                                             \
+    if (e_ != cudaSuccess) {                                             \
+      set_error(#expr, cudaGetErrorString(e_));                          \
+      return fail(e_ == cudaErrorMemoryAllocation ? CJM_ERR_OOM : CJM_ERR_CUDA); \
+    }                                                                    \
+  } while (0)
+
+  int dev = opt.device;
+  if (dev < 0) PLAN_CUDA(cudaGetDevice(&dev));
+  pl->device = dev;
+  PLAN_CUDA(cudaSetDevice(dev));
+  int nsm = 0;
+  PLAN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+
+  // ---- launch configuration
+  pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 2;
+  if (opt.tile_w) {
+    pl->W = opt.tile_w;
+  } else {
+    // prefer 256-wide strips unless that leaves fewer than ~48 rows per CTA
+    const long long strips256 = (nx + 255) / 256;
+    const long long rows_per_cta = strips256 * nyl / ((long long)nsm * pl->ctas_per_sm);
+    pl->W = rows_per_cta >= 48 ? 256 : 128;
+  }
+  pl->stages = opt.stages > 0 ? opt.stages : (pl->W == 256 ? 8 : 12);
+  pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 256;
+  const int UROW = pl->W + 8;
+  pl->smem = (size_t)pl->stages * (UROW + pl->W) * sizeof(double) + 2 * pl->stages * sizeof(uint64_t);
+  for (int mode = 0; mode < 3; ++mode) {
+    KernelFn k = pick_kernel(stencil, pl->W, mode);
+    PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)pl->smem));
+  }
+  int occ = 0;
+  PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ, (const void*)pick_kernel(stencil, pl->W, MODE_CHECK), pl->W + 32, pl->smem));
+  if (occ < 1) return fail(CJM_ERR_INVALID_ARG);
+  pl->nctas = nsm * std::min(occ, pl->ctas_per_sm);
+
+  // ---- buffers: (ny_local + 2R) rows of pitch ld; interior column 0 at PADL
+  pl->ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
+  pl->buf_elems = (size_t)(nyl + 2 * R) * pl->ld;
+  pl->g_elems = (size_t)nyl * pl->ld;
+  PLAN_CUDA(cudaMalloc(&pl->buf[0], pl->buf_elems * sizeof(double)));
+  PLAN_CUDA(cudaMalloc(&pl->buf[1], pl->buf_elems * sizeof(double)));
+  PLAN_CUDA(cudaMalloc(&pl->G, pl->g_elems * sizeof(double)));
+  PLAN_CUDA(cudaMemset(pl->buf[0], 0, pl->buf_elems * sizeof(double)));
+  PLAN_CUDA(cudaMemset(pl->buf[1], 0, pl->buf_elems * sizeof(double)));
+  PLAN_CUDA(cudaMemset(pl->G, 0, pl->g_elems * sizeof(double)));
+  PLAN_CUDA(cudaMalloc(&pl->w_dev, (size_t)pl->P * sizeof(double)));
+  PLAN_CUDA(cudaMemcpy(pl->w_dev, pl->sched.w.data(), (size_t)pl->P * sizeof(double),
+                       cudaMemcpyHostToDevice));
+  PLAN_CUDA(cudaMalloc(&pl->partials, (size_t)pl->nctas * 2 * sizeof(double)));
+  PLAN_CUDA(cudaMalloc(&pl->result, 2 * sizeof(double)));
+  PLAN_CUDA(cudaMalloc(&pl->ctr, sizeof(unsigned long long)));
+  PLAN_CUDA(cudaMalloc(&pl->ticket, sizeof(unsigned int)));
+  PLAN_CUDA(cudaMemset(pl->ctr, 0, sizeof(unsigned long long)));
+  PLAN_CUDA(cudaMemset(pl->ticket, 0, sizeof(unsigned int)));
+  PLAN_CUDA(cudaMallocHost(&pl->result_host, 2 * sizeof(double)));
+  PLAN_CUDA(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
+  for (auto& e : pl->ev) PLAN_CUDA(cudaEventCreate(&e));
+
+  if (pl->world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, opt.nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&pl->comm, pl->world, id, pl->rank);
+    if (r != ncclSuccess) {
+      set_error("ncclCommInitRank", ncclGetErrorString(r));
+      return fail(CJM_ERR_NCCL);
+    }
+  }
+  PLAN_CUDA(cudaDeviceSynchronize());
+#undef PLAN_CUDA
+  pl->plan_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = pl;
+  return CJM_OK;
+}
+
+cjm_status cjm_plan_info(cjm_plan_t p, cjm_report* info, int* reach, int* y0, int* ny_local,
+                         const double** host_weights) {
+  if (!p) return CJM_ERR_INVALID_ARG;
+  if (info) fill_static(p, info);
+  if (reach) *reach = p->R;
+  if (y0) *y0 = p->y0;
+  if (ny_local) *ny_local = p->ny_local;
+  if (host_weights) *host_weights = p->sched.w.data();
+  return CJM_OK;
+}
+
+cjm_status cjm_solve(cjm_plan_t p, const double* rhs, long long ld_rhs, double* u, long long ld_u,
+                     void* cuda_stream, cjm_report* rep) {
+  return solve_impl(p, rhs, ld_rhs, u, ld_u, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice,
+                    cuda_stream, rep);
+}
+
+cjm_status cjm_solve_host(cjm_plan_t p, const double* rhs_host, long long ld_rhs, double* u_host,
+                          long long ld_u, void* cuda_stream, cjm_report* rep) {
+  return solve_impl(p, rhs_host, ld_rhs, u_host, ld_u, cudaMemcpyHostToDevice,
+                    cudaMemcpyDeviceToHost, cuda_stream, rep);
+}
+
+cjm_status cjm_sweeps(cjm_plan_t p, const double* rhs, long long ld_rhs, double* u, long long ld_u,
+                      long long first, long long count, void* cuda_stream, cjm_report* rep_out) {
+  if (!check_layout(p, rhs, ld_rhs, u, ld_u) || !rhs || first < 0 || count < 0) {
+    set_error("cjm_sweeps", "invalid argument");
+    return CJM_ERR_INVALID_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  cjm_report rep;
+  fill_static(p, &rep);
+  long long launches = 2;
+  STATUS_TRY(stage_in(p, rhs, ld_rhs, u, ld_u, true, cudaMemcpyDeviceToDevice, st));
+  STATUS_TRY(set_counter(p, (unsigned long long)first, st));
+  STATUS_TRY(halo_exchange(p, p->buf[first & 1], st));
+  CUDA_TRY(cudaEventRecord(p->ev[2], st));
+  STATUS_TRY(run_hot(p, first, count, st, &launches));
+  CUDA_TRY(cudaEventRecord(p->ev[3], st));
+  STATUS_TRY(stage_out(p, (int)((first + count) & 1), u, ld_u, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  rep.sweep_s = elapsed_s(p->ev[2], p->ev[3]);
+  rep.sweeps_timed = count;
+  rep.iterations = count;
+  rep.kernel_launches = launches;
+  if (rep_out) *rep_out = rep;
+  return CJM_OK;
+}
+
+cjm_status cjm_residual(cjm_plan_t p, const double* rhs, long long ld_rhs, const double* u,
+                        long long ld_u, void* cuda_stream, double* l2, double* linf) {
+  if (!check_layout(p, rhs, ld_rhs, u, ld_u) || !rhs) {
+    set_error("cjm_residual", "invalid argument");
+    return CJM_ERR_INVALID_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  STATUS_TRY(stage_in(p, rhs, ld_rhs, u, ld_u, false, cudaMemcpyDeviceToDevice, st));
+  STATUS_TRY(set_counter(p, 0ull, st));
+  STATUS_TRY(halo_exchange(p, p->buf[0], st));
+  long long launches = 0;
+  double s, m;
+  STATUS_TRY(check_sweep(p, MODE_RESID, 0, st, &s, &m, &launches));
+  const double sc = std::fabs(p->gscale);
+  if (l2) *l2 = std::sqrt(s) / sc;
+  if (linf) *linf = m / sc;
+  return CJM_OK;
+}
+
+const char* cjm_status_str(int s) {
+  switch (s) {
+    case CJM_OK: return "CJM_OK";
+    case CJM_ERR_INVALID_ARG: return "CJM_ERR_INVALID_ARG";
+    case CJM_ERR_UNSUPPORTED: return "CJM_ERR_UNSUPPORTED";
+    case CJM_ERR_NOT_CONVERGED: return "CJM_ERR_NOT_CONVERGED";
+    case CJM_ERR_DIVERGED: return "CJM_ERR_DIVERGED";
+    case CJM_ERR_STAGNATED: return "CJM_ERR_STAGNATED";
+    case CJM_ERR_CUDA: return "CJM_ERR_CUDA";
+    case CJM_ERR_NCCL: return "CJM_ERR_NCCL";
+    case CJM_ERR_OOM: return "CJM_ERR_OOM";
+    default: return "CJM_ERR_UNKNOWN";
+  }
+}
+
+const char* cjm_last_error(void) { return g_last_error.c_str(); }
+
+int cjm_version(void) { return 100 * CJM_VERSION_MAJOR + CJM_VERSION_MINOR; }
+
+}  // extern "C"

@@ -1,0 +1,26 @@
+// Internal declarations of libcjm (not part of the C ABI).
+#pragma once
+
+#include <vector>
+
+namespace cjm {
+
+// Interior column 0 of every internal row sits at column PADL: 32-byte aligned
+// stores, 16-byte aligned TMA row loads starting at column PADL - 2.
+constexpr int PADL = 4;
+
+struct Schedule {
+  double kmin = 0, kmax = 0;
+  long long m_min = 0, P = 0;
+  std::vector<long long> t;  // Chebyshev zero index per sweep position
+  std::vector<double> w;     // weight per sweep position
+};
+
+int stencil_reach(int stencil);
+bool spectral_bounds(int stencil, int nx, int ny, double* kmin, double* kmax);
+long long chebyshev_degree(double kmin, double kmax, double tol);
+long long smooth_cycle_length(long long m, int* a_out, int* b_out);
+std::vector<long long> lebedev23_order(int a, int b);
+bool build_schedule(int stencil, int nx, int ny, double tol, int order, Schedule* s);
+
+}  // namespace cjm

@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path (called through the C ABI) against the oracle.
+
+Bar (BASELINE.json north_star): the same iteration count, and the final field
+within max|du| <= 1e-10 max|u|.  Because kernel and oracle evaluate the same
+per-point association (DESIGN R6) with the same weights (bitwise-equal
+schedulers, tests/test_abi.py), we additionally expect -- and assert --
+bitwise equality of every field.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import ROOT
+from paper_1705_00103_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1705_00103_b200 import cjm  # noqa: E402
+
+DIGESTS = os.path.join(ROOT, "tests", "golden", "oracle_digests.json")
+REL = 1e-10
+
+
+def dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def host(t) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def assert_field_parity(got: np.ndarray, want: np.ndarray, r: int):
+    gi, wi = got[r:-r, r:-r], want[r:-r, r:-r]
+    scale = max(np.max(np.abs(wi)), 1e-300)
+    err = np.max(np.abs(gi - wi)) / scale
+    assert err <= REL, f"max|du|/max|u| = {err:.3e}"
+    assert np.array_equal(gi, wi), f"not bitwise (max rel diff {err:.3e})"
+    # ghosts never written
+    assert np.array_equal(got[:r], want[:r]) and np.array_equal(got[-r:], want[-r:])
+    assert np.array_equal(got[:, :r], want[:, :r]) and np.array_equal(got[:, -r:], want[:, -r:])
+
+
+# ------------------------------------------------------------ single sweeps
+SHAPES = [(8, 8), (64, 64), (100, 37), (257, 300), (513, 70), (1000, 11), (4, 4), (5, 9)]
+
+
+@pytest.mark.parametrize("stencil", (5, 9, 17))
+@pytest.mark.parametrize("nx,ny", SHAPES)
+@pytest.mark.parametrize("tile_w", (128, 256))
+def test_one_sweep_bitwise(stencil, nx, ny, tile_w):
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=inputs.SEED_BASE + nx + 7 * ny)
+    with cjm.Plan(stencil, nx, ny, h, 1e-8, tile_w=tile_w) as plan:
+        w = plan.info()["weights"]
+        g = oracle.rhs_to_g(stencil, h, b)
+        for first in (0, 1, plan.P - 1):
+            ud = dev(u0)
+            plan.sweeps(dev(b), ud, first, 1)
+            torch.cuda.synchronize()
+            want = oracle.sweep(stencil, u0, g, w[first % plan.P])
+            assert_field_parity(host(ud), want, r)
+
+
+@pytest.mark.parametrize("stencil", (5, 9, 17))
+@pytest.mark.parametrize("nx,ny,count", [(300, 257, 37), (1030, 515, 20), (64, 64, 324)])
+def test_sweep_segment_bitwise(stencil, nx, ny, count):
+    """A run of sweeps through the CUDA-graph hot loop (spans several graph
+    chunks when count > graph_chunk) vs the oracle sweep by sweep."""
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=3)
+    with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=16) as plan:
+        w = plan.info()["weights"]
+        ud = dev(u0)
+        plan.sweeps(dev(b), ud, 5, count)
+        g = oracle.rhs_to_g(stencil, h, b)
+        u = u0
+        for k in range(count):
+            u = oracle.sweep(stencil, u, g, w[(5 + k) % plan.P])
+        assert_field_parity(host(ud), u, r)
+
+
+@pytest.mark.parametrize("cfg", [dict(tile_w=128, stages=4, ctas_per_sm=1),
+                                 dict(tile_w=256, stages=16, ctas_per_sm=3),
+                                 dict(tile_w=128, stages=32, ctas_per_sm=2, graph_chunk=7)])
+def test_launch_configuration_does_not_change_result(cfg):
+    nx, ny = 777, 301
+    u0, b, h = inputs.test_problem(nx, ny, 1, init="random", seed=5)
+    outs = []
+    for kw in (dict(), cfg):
+        with cjm.Plan(9, nx, ny, h, 1e-8, **kw) as plan:
+            ud = dev(u0)
+            plan.sweeps(dev(b), ud, 0, 40)
+            outs.append(host(ud))
+    assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------------------------------------------ residual
+@pytest.mark.parametrize("stencil", (5, 9, 17))
+def test_residual_matches_oracle(stencil):
+    r = oracle.reach(stencil)
+    nx, ny = 333, 129
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=8)
+    with cjm.Plan(stencil, nx, ny, h, 1e-8) as plan:
+        l2, li = plan.residual(dev(b), dev(u0))
+    ol2, oli = oracle.residual(stencil, h, b, u0)
+    assert l2 == pytest.approx(ol2, rel=1e-12)
+    assert li == oli   # max is order-free: bitwise
+
+
+# ------------------------------------------------------------ full solves
+@pytest.mark.parametrize("stencil", (5, 9, 17))
+@pytest.mark.parametrize("n,init", [(64, "zero"), (64, "random"), (200, "zero"), (129, "random")])
+def test_solve_matches_oracle(stencil, n, init):
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(n, n, r, init=init)
+    uo, ro = oracle.solve(stencil, h, 1e-8, b, u0)
+    with cjm.Plan(stencil, n, n, h, 1e-8) as plan:
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud)
+    assert rep["status"] == "CJM_OK" and ro["status"] == "OK"
+    assert rep["iterations"] == ro["iterations"] and rep["cycles"] == ro["cycles"]
+    assert rep["r0_l2"] == pytest.approx(ro["r0_l2"], rel=1e-12)
+    assert rep["r_l2"] == pytest.approx(ro["r_l2"], rel=1e-9)
+    assert_field_parity(host(ud), uo, r)
+
+
+def test_solve_nonsquare_ragged():
+    nx, ny = 301, 157
+    u0, b, h = inputs.test_problem(nx, ny, 2)
+    uo, ro = oracle.solve(17, h, 1e-8, b, u0)
+    with cjm.Plan(17, nx, ny, h, 1e-8) as plan:
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud)
+    assert rep["iterations"] == ro["iterations"]
+    assert_field_parity(host(ud), uo, 2)
+
+
+def test_solve_host_equals_solve_device():
+    n = 200
+    u0, b, h = inputs.test_problem(n, n, 1)
+    with cjm.Plan(9, n, n, h, 1e-8) as plan:
+        ud = dev(u0)
+        rd = plan.solve(dev(b), ud)
+        uh = u0.copy()
+        rh = plan.solve_host(b, uh)
+    assert rd["iterations"] == rh["iterations"]
+    assert np.array_equal(host(ud), uh)
+    assert rh["h2d_bytes"] == (u0.size + b.size) * 8 and rh["d2h_bytes"] == b.size * 8
+
+
+def test_zero_residual_returns_immediately():
+    u0 = np.zeros((66, 66))
+    b = np.zeros((64, 64))
+    with cjm.Plan(9, 64, 64, 1 / 65, 1e-8) as plan:
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud)
+    assert rep["status"] == "CJM_OK" and rep["iterations"] == 0 and rep["r0_l2"] == 0.0
+
+
+def test_ascending_order_fails_like_oracle():
+    n = 63
+    u0, b, h = inputs.test_problem(n, n, 1)
+    s = oracle.schedule(9, n, n, 1e-8)
+    _, ro = oracle.solve(9, h, 1e-8, b, u0, weights_override=np.sort(s["w"]))
+    with cjm.Plan(9, n, n, h, 1e-8, order=cjm.ORDER_ASCENDING) as plan:
+        rep = plan.solve(dev(b), dev(u0), ok=(0, 3, 4, 5))
+    assert rep["status"] != "CJM_OK" and ro["status"] != "OK"
+
+
+def test_jacobi_method_matches_oracle_sweeps():
+    """Classical Jacobi (w = 1, the paper's baseline P:298-300) through the same kernel."""
+    n = 48
+    u0, b, h = inputs.test_problem(n, n, 1)
+    with cjm.Plan(5, n, n, h, 1e-3, method=cjm.METHOD_JACOBI, jacobi_check=100, max_cycles=3) as plan:
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud, ok=(0, 3))
+    g = oracle.rhs_to_g(5, h, b)
+    u = u0
+    for _ in range(rep["iterations"]):
+        u = oracle.sweep(5, u, g, 1.0)
+    assert rep["iterations"] == 300
+    assert_field_parity(host(ud), u, 1)
+
+
+def test_bad_pitch_is_invalid_arg():
+    u0, b, h = inputs.test_problem(64, 64, 1)
+    with cjm.Plan(9, 64, 64, h, 1e-8) as plan:
+        ud = dev(u0)[:, :60]
+        with pytest.raises(cjm.CJMError) as e:
+            plan.solve(dev(b), ud)
+        assert e.value.name == "CJM_ERR_INVALID_ARG"
+
+
+# ------------------------------------------------------------ stored oracle solves
+def _digest_cases():
+    if not os.path.exists(DIGESTS):
+        return []
+    with open(DIGESTS) as f:
+        return sorted(json.load(f).keys())
+
+
+@pytest.mark.parametrize("name", _digest_cases())
+def test_solve_matches_stored_oracle_digest(name):
+    """Full solves at BASELINE sizes vs the oracle's stored result
+    (tests/make_oracle_digests.py): same iterations, sampled nodes within
+    1e-10 max|u| and bitwise, and the SHA-256 of the whole interior."""
+    with open(DIGESTS) as f:
+        rec = json.load(f)[name]
+    st, nx, ny, h, tol = rec["stencil"], rec["nx"], rec["ny"], rec["h"], rec["tol"]
+    free = torch.cuda.mem_get_info()[0]
+    if free < 9 * (nx + 4) * (ny + 4) * 8:
+        pytest.skip("not enough device memory")
+    r = oracle.reach(st)
+    u0, b, h2 = inputs.test_problem(nx, ny, r, init=rec["init"])
+    assert h2 == h
+    with cjm.Plan(st, nx, ny, h, tol) as plan:
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud)
+    assert rep["status"] == "CJM_OK"
+    assert rep["iterations"] == rec["report"]["iterations"]
+    u = host(ud)[r:r + ny, r:r + nx]
+    flat = u.ravel()
+    idx = np.array(rec["sample_index"])
+    want = np.array([float.fromhex(v) for v in rec["sample_hex"]])
+    err = np.max(np.abs(flat[idx] - want)) / rec["max_abs_u"]
+    assert err <= REL
+    assert np.array_equal(flat[idx], want)
+    assert np.max(np.abs(u)) == rec["max_abs_u"]
+    assert hashlib.sha256(np.ascontiguousarray(u, dtype="<f8").tobytes()).hexdigest() == rec["sha256"]

@@ -409,3 +409,14 @@ def test_invalid_arguments():
     for args in [(9, h, 0.0), (9, h, 1.0), (9, -h, 1e-8), (7, h, 1e-8)]:
         _, rep = oracle.solve(args[0], args[1], args[2], b, u0)
         assert rep["status"] == "INVALID"
+
+
+def test_sweeps_segment_equals_repeated_sweep():
+    n = 37
+    u0, b, h = inputs.test_problem(n, n + 3, 2, init="random")
+    s = oracle.schedule(17, n, n + 3, 1e-8)
+    g = oracle.rhs_to_g(17, h, b)
+    u = u0
+    for k in range(11):
+        u = oracle.sweep(17, u, g, s["w"][(s["P"] - 4 + k) % s["P"]])
+    assert np.array_equal(oracle.sweeps(17, u0, g, s["w"], s["P"] - 4, 11), u)
