@@ -197,8 +197,17 @@ class Plan:
                  weights=np.ctypeslib.as_array(w, shape=(rep.cycle_len,)).copy())
         return d
 
+    def _check_shapes(self, rhs, u):
+        r = self.reach
+        if tuple(u.shape) != (self.ny_local + 2 * r, self.nx + 2 * r):
+            raise ValueError(f"u: shape {tuple(u.shape)}, plan expects "
+                             f"{(self.ny_local + 2 * r, self.nx + 2 * r)}")
+        if tuple(rhs.shape) != (self.ny_local, self.nx):
+            raise ValueError(f"rhs: shape {tuple(rhs.shape)}, plan expects {(self.ny_local, self.nx)}")
+
     def solve(self, rhs, u, stream=None, ok=(0,)) -> dict:
         """cjm_solve on device tensors; u is updated in place."""
+        self._check_shapes(rhs, u)
         rp, rl = _dev_ptr(rhs, "rhs")
         up, ul = _dev_ptr(u, "u")
         rep = Report()
@@ -207,6 +216,7 @@ class Plan:
 
     def solve_host(self, rhs, u, stream=None, ok=(0,)) -> dict:
         """cjm_solve_host on host arrays; u is updated in place."""
+        self._check_shapes(rhs, u)
         rp, rl = _host_ptr(rhs, "rhs")
         up, ul = _host_ptr(u, "u")
         rep = Report()
@@ -215,6 +225,7 @@ class Plan:
         return rep.as_dict()
 
     def sweeps(self, rhs, u, first: int, count: int, stream=None) -> dict:
+        self._check_shapes(rhs, u)
         rp, rl = _dev_ptr(rhs, "rhs")
         up, ul = _dev_ptr(u, "u")
         rep = Report()
@@ -223,6 +234,7 @@ class Plan:
         return rep.as_dict()
 
     def residual(self, rhs, u, stream=None) -> tuple[float, float]:
+        self._check_shapes(rhs, u)
         rp, rl = _dev_ptr(rhs, "rhs")
         up, ul = _dev_ptr(u, "u")
         l2, li = C.c_double(), C.c_double()

@@ -1,0 +1,54 @@
+"""Run a fixed number of scheduled sweeps of one config (for ncu and tuning).
+
+    python scripts/sweep_runner.py --config cjm9_4096 --count 30 [--tile-w 256 --stages 8 --ctas-per-sm 2]
+    python scripts/sweep_runner.py --tune        # sweep the launch-configuration grid
+"""
+import argparse
+import itertools
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from bench import CONFIGS, make_problem  # noqa: E402
+from paper_1705_00103_b200 import cjm  # noqa: E402
+
+
+def run(config, count, warm, **kw):
+    st, nx, ny, tol, _ = CONFIGS[config]
+    u0, b, h = make_problem(st, nx, ny, 0, ny)
+    ud, bd = torch.from_numpy(u0).cuda(), torch.from_numpy(b).cuda()
+    with cjm.Plan(st, nx, ny, h, tol, **kw) as plan:
+        if warm:
+            plan.sweeps(bd, ud, 1, warm)
+        rep = plan.sweeps(bd, ud, 1, count)
+    us = 1e6 * rep["sweep_s"] / count
+    return dict(config=config, **kw, us_per_sweep=us, gbs=24.0 * nx * ny / (us * 1e-6) / 1e9)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cjm9_4096")
+    ap.add_argument("--count", type=int, default=30)
+    ap.add_argument("--warm", type=int, default=0)
+    ap.add_argument("--tile-w", type=int, default=0)
+    ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--tune", action="store_true")
+    a = ap.parse_args()
+    if a.tune:
+        for cfgname in a.config.split(","):
+            for tw, stg, cps in itertools.product((128, 256), (4, 8, 12, 16), (1, 2, 3, 4)):
+                try:
+                    print(json.dumps(run(cfgname, 2000, 200, tile_w=tw, stages=stg, ctas_per_sm=cps)),
+                          flush=True)
+                except Exception as e:  # noqa: BLE001
+                    print(json.dumps(dict(config=cfgname, tile_w=tw, stages=stg, ctas_per_sm=cps,
+                                          error=str(e))), flush=True)
+    else:
+        print(json.dumps(run(a.config, a.count, a.warm, tile_w=a.tile_w, stages=a.stages,
+                             ctas_per_sm=a.ctas_per_sm)))

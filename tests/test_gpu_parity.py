@@ -195,10 +195,12 @@ def test_jacobi_method_matches_oracle_sweeps():
 def test_bad_pitch_is_invalid_arg():
     u0, b, h = inputs.test_problem(64, 64, 1)
     with cjm.Plan(9, 64, 64, h, 1e-8) as plan:
-        ud = dev(u0)[:, :60]
+        narrow = torch.zeros(66, 60, dtype=torch.float64, device="cuda")   # pitch 60 < nx + 2r
         with pytest.raises(cjm.CJMError) as e:
-            plan.solve(dev(b), ud)
+            plan.solve(dev(b), narrow)
         assert e.value.name == "CJM_ERR_INVALID_ARG"
+        with pytest.raises(ValueError):       # shape checked by the binding
+            plan.solve(dev(b), dev(u0)[:, :60])
 
 
 # ------------------------------------------------------------ stored oracle solves
