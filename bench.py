@@ -199,6 +199,7 @@ def main():
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--graph-chunk", type=int, default=0)
+    ap.add_argument("--temporal-k", type=int, default=0)
     args = ap.parse_args()
 
     world = env_int("WORLD_SIZE", 1)
@@ -228,7 +229,8 @@ def main():
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
     opts = dict(device=local_rank, world_size=world, rank=rank, tile_w=args.tile_w,
-                stages=args.stages, ctas_per_sm=args.ctas_per_sm, graph_chunk=args.graph_chunk)
+                stages=args.stages, ctas_per_sm=args.ctas_per_sm, graph_chunk=args.graph_chunk,
+                temporal_k=args.temporal_k)
     stream = torch.cuda.current_stream()
     u_dev0 = torch.from_numpy(u0).to(dev)
     b_dev = torch.from_numpy(b).to(dev)

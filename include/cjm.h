@@ -93,7 +93,9 @@ typedef struct {
                               broadcast by the caller; required when world_size > 1 */
     int device;            /* CUDA device ordinal; -1 (default) = current device */
     /* tuning knobs, 0 = automatic */
-    int tile_w;            /* columns per CTA strip: 128 or 256 */
+    int temporal_k;        /* sweeps fused per kernel launch (temporal blocking,
+                              SURVEY NEXT-1), 1..4; multi-GPU plans use 1 */
+    int tile_w;            /* tile columns per CTA: 256 or 512 */
     int ctas_per_sm;       /* resident CTAs per SM of the persistent sweep grid */
     int stages;            /* depth of the TMA row ring */
     int graph_chunk;       /* sweeps captured per CUDA graph */
@@ -113,6 +115,8 @@ typedef struct {
     double sweep_s;        /* device seconds of the non-check sweeps (CUDA events) */
     long long sweeps_timed;/* number of sweeps inside sweep_s */
     long long kernel_launches; /* kernels of this library launched by the call */
+    long long hot_launches;    /* sweep-kernel launches inside sweep_s */
+    int temporal_k;            /* sweeps per hot launch */
     double h2d_bytes, d2h_bytes;  /* host<->device bytes moved by the call */
 } cjm_report;
 

@@ -44,7 +44,8 @@ class CJMError(RuntimeError):
 class Options(C.Structure):
     _fields_ = [("max_cycles", C.c_int), ("order", C.c_int), ("method", C.c_int),
                 ("jacobi_check", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
-                ("nccl_id", C.c_void_p), ("device", C.c_int), ("tile_w", C.c_int),
+                ("nccl_id", C.c_void_p), ("device", C.c_int), ("temporal_k", C.c_int),
+                ("tile_w", C.c_int),
                 ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int)]
 
 
@@ -56,6 +57,7 @@ class Report(C.Structure):
                 ("r_l2", C.c_double), ("r_linf", C.c_double),
                 ("plan_s", C.c_double), ("solve_s", C.c_double), ("sweep_s", C.c_double),
                 ("sweeps_timed", C.c_longlong), ("kernel_launches", C.c_longlong),
+                ("hot_launches", C.c_longlong), ("temporal_k", C.c_int),
                 ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double)]
 
     def as_dict(self) -> dict:

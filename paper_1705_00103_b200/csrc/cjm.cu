@@ -62,29 +62,46 @@ enum Mode { MODE_HOT = 0, MODE_CHECK = 1, MODE_RESID = 2 };
 
 using KernelFn = void (*)(const cjm::SweepParams);
 
-template <int ST, int W>
+template <int ST, int NT, int K>
 KernelFn pick_mode(int mode) {
   switch (mode) {
-    case MODE_HOT: return cjm::cjm_sweep_kernel<ST, W, false, true>;
-    case MODE_CHECK: return cjm::cjm_sweep_kernel<ST, W, true, true>;
-    default: return cjm::cjm_sweep_kernel<ST, W, true, false>;
+    case MODE_HOT: return cjm::cjm_sweep_kernel<ST, NT, K, false, true>;
+    case MODE_CHECK: return cjm::cjm_sweep_kernel<ST, NT, K, true, true>;
+    default: return cjm::cjm_sweep_kernel<ST, NT, 1, true, false>;
+  }
+}
+
+template <int ST, int NT>
+KernelFn pick_k(int K, int mode) {
+  switch (K) {
+    case 1: return pick_mode<ST, NT, 1>(mode);
+    case 2: return pick_mode<ST, NT, 2>(mode);
+    case 3: return pick_mode<ST, NT, 3>(mode);
+    default: return pick_mode<ST, NT, 4>(mode);
   }
 }
 
 template <int ST>
-KernelFn pick_w(int W, int mode) {
-  return W == 128 ? pick_mode<ST, 128>(mode) : pick_mode<ST, 256>(mode);
+KernelFn pick_nt(int NT, int K, int mode) {
+  return NT == 256 ? pick_k<ST, 256>(K, mode) : pick_k<ST, 128>(K, mode);
 }
 
-KernelFn pick_kernel(int stencil, int W, int mode) {
+KernelFn pick_kernel(int stencil, int NT, int K, int mode) {
   switch (stencil) {
-    case 5: return pick_w<5>(W, mode);
-    case 9: return pick_w<9>(W, mode);
-    default: return pick_w<17>(W, mode);
+    case 5: return pick_nt<5>(NT, K, mode);
+    case 9: return pick_nt<9>(NT, K, mode);
+    default: return pick_nt<17>(NT, K, mode);
   }
 }
 
-__global__ void set_counter_kernel(unsigned long long* ctr, unsigned long long v) { *ctr = v; }
+// halo columns lost per side by K-1 on-chip levels (mirror of TileGeom::E)
+int tile_e(int R, int K) { return K == 1 ? 0 : ((R * (K - 1) + 1) & ~1); }
+
+__global__ void set_state_kernel(cjm::SweepState* st, unsigned long long n) {
+  st->n = n;
+  st->cur = 0u;
+  st->ticket = 0u;
+}
 
 }  // namespace
 
@@ -107,41 +124,49 @@ struct cjm_plan_s {
   double* partials = nullptr;
   double* result = nullptr;
   double* result_host = nullptr;  // pinned, 2 doubles
-  unsigned long long* ctr = nullptr;
-  unsigned int* ticket = nullptr;
+  cjm::SweepState* state = nullptr;
   // launch configuration
-  int W = 256, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 256;
-  size_t smem = 0;
+  int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
   cudaStream_t cap_stream = nullptr;
   std::map<std::pair<long long, int>, cudaGraphExec_t> graphs;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double plan_s = 0;
+  // host mirror of the device state during a call
+  int host_cur = 0;
+  long long launches = 0;
 };
 
 namespace {
 
-cjm_status launch_sweep(cjm_plan_s* pl, int mode, cudaStream_t st) {
+size_t smem_bytes(const cjm_plan_s* pl, int K) {
+  const int T = 2 * pl->NT, ROW = T + 8;
+  return (size_t)pl->stages * (ROW + T) * sizeof(double) +
+         (size_t)(K - 1) * 2 * ROW * sizeof(double) + 2 * (size_t)pl->stages * sizeof(uint64_t);
+}
+
+// One sweep-kernel launch of K fused sweeps reading buffer host_cur.
+cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
   cjm::SweepParams sp;
-  sp.buf0 = pl->buf[0];
-  sp.buf1 = pl->buf[1];
+  sp.buf[0] = pl->buf[0];
+  sp.buf[1] = pl->buf[1];
   sp.g = pl->G;
   sp.w = pl->w_dev;
-  sp.ctr = pl->ctr;
-  sp.ticket = pl->ticket;
+  sp.state = pl->state;
   sp.partials = pl->partials;
   sp.result = pl->result;
   sp.P = pl->P;
   sp.ld = pl->ld;
   sp.nx = pl->nx;
   sp.rows = pl->ny_local;
-  sp.row0 = 0;
   sp.stages = pl->stages;
-  sp.advance = 1;
-  const long long nstrips = (pl->nx + pl->W - 1) / pl->W;
+  const int tout = 2 * pl->NT - 2 * tile_e(pl->R, K);
+  const long long nstrips = (pl->nx + tout - 1) / tout;
   sp.units = nstrips * pl->ny_local;
-  KernelFn k = pick_kernel(pl->stencil, pl->W, mode);
-  k<<<pl->nctas, pl->W + 32, pl->smem, st>>>(sp);
+  KernelFn k = pick_kernel(pl->stencil, pl->NT, K, mode);
+  k<<<pl->nctas, pl->NT + 32, smem_bytes(pl, K), st>>>(sp);
   CUDA_TRY(cudaGetLastError());
+  pl->launches += 1;
+  if (mode != MODE_RESID) pl->host_cur ^= 1;
   return CJM_OK;
 }
 
@@ -167,54 +192,65 @@ cjm_status halo_exchange(cjm_plan_s* pl, double* b, cudaStream_t st) {
   return CJM_OK;
 }
 
-// One hot sweep reading buffer parity `par` (= n & 1) then the halo exchange
-// of its output.
-cjm_status hot_sweep(cjm_plan_s* pl, int par, cudaStream_t st) {
-  STATUS_TRY(launch_sweep(pl, MODE_HOT, st));
-  return halo_exchange(pl, pl->buf[par ^ 1], st);
+// A sweep launch followed by the halo exchange of its output (multi-GPU).
+cjm_status sweep_and_exchange(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
+  STATUS_TRY(launch_sweep(pl, mode, K, st));
+  return halo_exchange(pl, pl->buf[pl->host_cur], st);
 }
 
-cjm_status get_graph(cjm_plan_s* pl, long long len, int par, cudaGraphExec_t* out) {
-  const int key_par = pl->world > 1 ? par : 0;   // single GPU: buffers resolved on device
-  auto it = pl->graphs.find({len, key_par});
+// Graph of `len` hot launches of K sweeps each.  Single GPU: every launch has
+// identical parameters (buffers resolved on the device), one graph per length.
+// Multi-GPU: the NCCL buffers depend on the starting buffer parity.
+cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out) {
+  const int par = pl->world > 1 ? pl->host_cur : 0;
+  const std::pair<long long, int> key{len * 8 + K, par};
+  auto it = pl->graphs.find(key);
   if (it != pl->graphs.end()) { *out = it->second; return CJM_OK; }
+  const int saved_cur = pl->host_cur;
+  const long long saved_launches = pl->launches;
   cudaGraph_t graph = nullptr;
   CUDA_TRY(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
   cjm_status s = CJM_OK;
-  for (long long k = 0; k < len && s == CJM_OK; ++k) s = hot_sweep(pl, (int)((par + k) & 1), pl->cap_stream);
+  for (long long k = 0; k < len && s == CJM_OK; ++k) s = sweep_and_exchange(pl, MODE_HOT, K, pl->cap_stream);
   cudaError_t e = cudaStreamEndCapture(pl->cap_stream, &graph);
+  pl->host_cur = saved_cur;
+  pl->launches = saved_launches;
   if (s != CJM_OK) { if (graph) cudaGraphDestroy(graph); return s; }
   CUDA_TRY(e);
   cudaGraphExec_t exec = nullptr;
   e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
   CUDA_TRY(e);
-  pl->graphs[{len, key_par}] = exec;
+  pl->graphs[key] = exec;
   *out = exec;
   return CJM_OK;
 }
 
-// Run `count` hot sweeps starting at global sweep index n0 (host-tracked).
-cjm_status run_hot(cjm_plan_s* pl, long long n0, long long count, cudaStream_t st,
-                   long long* launches) {
-  long long done = 0;
-  while (done < count) {
-    const long long len = std::min<long long>(pl->graph_chunk, count - done);
+// Run `count` hot sweeps: blocks of K fused sweeps from CUDA graphs, the
+// remainder (< K) as single-sweep launches.  Returns the hot launch count.
+cjm_status run_hot(cjm_plan_s* pl, long long count, cudaStream_t st, long long* hot_launches) {
+  const int K = pl->K;
+  long long blocks = count / K;
+  const long long rem = count % K;
+  while (blocks > 0) {
+    const long long len = std::min<long long>(pl->graph_chunk, blocks);
     cudaGraphExec_t ex;
-    STATUS_TRY(get_graph(pl, len, (int)((n0 + done) & 1), &ex));
+    STATUS_TRY(get_graph(pl, len, K, &ex));
     CUDA_TRY(cudaGraphLaunch(ex, st));
-    done += len;
-    *launches += len;
+    pl->host_cur ^= (int)(len & 1);
+    pl->launches += len;
+    *hot_launches += len;
+    blocks -= len;
+  }
+  for (long long r = 0; r < rem; ++r) {
+    STATUS_TRY(sweep_and_exchange(pl, MODE_HOT, 1, st));
+    *hot_launches += 1;
   }
   return CJM_OK;
 }
 
-// Check sweep (fused reduction) + global sum/max + D2H of the two scalars.
-cjm_status check_sweep(cjm_plan_s* pl, int mode, long long n, cudaStream_t st, double* s, double* m,
-                       long long* launches) {
-  STATUS_TRY(launch_sweep(pl, mode, st));
-  *launches += 1;
-  if (mode == MODE_CHECK) STATUS_TRY(halo_exchange(pl, pl->buf[(n & 1) ^ 1], st));
+// Sum / max over ranks of the reduction result and D2H of the two scalars.
+cjm_status fetch_result(cjm_plan_s* pl, cudaStream_t st, double* s, double* m) {
   if (pl->world > 1) {
     NCCL_TRY(ncclGroupStart());
     NCCL_TRY(ncclAllReduce(pl->result, pl->result, 1, ncclDouble, ncclSum, pl->comm, st));
@@ -228,9 +264,11 @@ cjm_status check_sweep(cjm_plan_s* pl, int mode, long long n, cudaStream_t st, d
   return CJM_OK;
 }
 
-cjm_status set_counter(cjm_plan_s* pl, unsigned long long v, cudaStream_t st) {
-  set_counter_kernel<<<1, 1, 0, st>>>(pl->ctr, v);
+cjm_status set_state(cjm_plan_s* pl, unsigned long long n, cudaStream_t st) {
+  set_state_kernel<<<1, 1, 0, st>>>(pl->state, n);
   CUDA_TRY(cudaGetLastError());
+  pl->host_cur = 0;
+  pl->launches += 1;
   return CJM_OK;
 }
 
@@ -252,6 +290,7 @@ cjm_status stage_in(cjm_plan_s* pl, const double* rhs, long long ld_rhs, const d
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
     cjm::cjm_scale_kernel<<<blocks, 256, 0, st>>>(pl->G, pl->ld, pl->nx, pl->ny_local, pl->gscale);
     CUDA_TRY(cudaGetLastError());
+    pl->launches += 1;
   }
   return CJM_OK;
 }
@@ -284,9 +323,10 @@ void fill_static(const cjm_plan_s* pl, cjm_report* r) {
   r->kappa_min = pl->sched.kmin;
   r->kappa_max = pl->sched.kmax;
   r->plan_s = pl->plan_s;
+  r->temporal_k = pl->K;
 }
 
-// The whole solve (rows a5-a10); `kind` selects device or host user buffers.
+// The whole solve (rows a5-a10); `kin` / `kout` select device or host user buffers.
 cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, double* u,
                       long long ld_u, cudaMemcpyKind kin, cudaMemcpyKind kout, void* stream,
                       cjm_report* rep_out) {
@@ -299,28 +339,30 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
   cjm_report rep;
   fill_static(pl, &rep);
   const double sc = std::fabs(pl->gscale);
-  long long launches = 0;
+  pl->launches = 0;
+  // the check launch fuses Kc sweeps; the hot part of a cycle is P - Kc sweeps
+  const int Kc = (int)std::min<long long>(pl->K, pl->P);
 
   CUDA_TRY(cudaEventRecord(pl->ev[0], st));
   STATUS_TRY(stage_in(pl, rhs, ld_rhs, u, ld_u, true, kin, st));
-  launches += 1;
   if (kin == cudaMemcpyHostToDevice) {
     rep.h2d_bytes = (double)(pl->ny_local + 2 * pl->R) * (pl->nx + 2 * pl->R) * 8.0 +
                     (double)pl->ny_local * pl->nx * 8.0;
   }
-  STATUS_TRY(set_counter(pl, 0ull, st));
-  launches += 1;
+  STATUS_TRY(set_state(pl, 0ull, st));
   STATUS_TRY(halo_exchange(pl, pl->buf[0], st));
 
   double s, m;
-  STATUS_TRY(check_sweep(pl, MODE_CHECK, 0, st, &s, &m, &launches));
+  int check_in = pl->host_cur;           // buffer holding u_0
+  STATUS_TRY(sweep_and_exchange(pl, MODE_CHECK, Kc, st));
+  STATUS_TRY(fetch_result(pl, st, &s, &m));
   rep.r0_l2 = std::sqrt(s) / sc;
   rep.r0_linf = m / sc;
   rep.r_l2 = rep.r0_l2;
   rep.r_linf = rep.r0_linf;
 
   int status = CJM_ERR_NOT_CONVERGED;
-  long long n_out = 0;   // sweep index of the exported iterate
+  int out_buf = check_in;                 // buffer of the exported iterate
   if (rep.r0_l2 == 0.0) {
     status = CJM_OK;
   } else if (!std::isfinite(rep.r0_l2)) {
@@ -328,20 +370,20 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
   } else {
     double rho_prev = rep.r0_l2;
     for (int c = 1; c <= pl->max_cycles; ++c) {
-      const long long n0 = (long long)(c - 1) * pl->P + 1;
       CUDA_TRY(cudaEventRecord(pl->ev[2], st));
-      STATUS_TRY(run_hot(pl, n0, pl->P - 1, st, &launches));
+      STATUS_TRY(run_hot(pl, pl->P - Kc, st, &rep.hot_launches));
       CUDA_TRY(cudaEventRecord(pl->ev[3], st));
-      const long long n = (long long)c * pl->P;
-      STATUS_TRY(check_sweep(pl, MODE_CHECK, n, st, &s, &m, &launches));
+      check_in = pl->host_cur;            // holds u_{cP}
+      STATUS_TRY(sweep_and_exchange(pl, MODE_CHECK, Kc, st));
+      STATUS_TRY(fetch_result(pl, st, &s, &m));
       rep.sweep_s += elapsed_s(pl->ev[2], pl->ev[3]);
-      rep.sweeps_timed += pl->P - 1;
+      rep.sweeps_timed += pl->P - Kc;
       const double rho = std::sqrt(s) / sc;
       rep.cycles = c;
-      rep.iterations = n;
+      rep.iterations = (long long)c * pl->P;
       rep.r_l2 = rho;
       rep.r_linf = m / sc;
-      n_out = n;
+      out_buf = check_in;
       if (!std::isfinite(rho)) { status = CJM_ERR_DIVERGED; break; }
       if (rho <= pl->tol * rep.r0_l2) { status = CJM_OK; break; }
       if (pl->method == CJM_METHOD_CHEBYSHEV && rho > 0.5 * rho_prev) {
@@ -351,12 +393,12 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
       rho_prev = rho;
     }
   }
-  STATUS_TRY(stage_out(pl, (int)(n_out & 1), u, ld_u, kout, st));
+  STATUS_TRY(stage_out(pl, out_buf, u, ld_u, kout, st));
   if (kout == cudaMemcpyDeviceToHost) rep.d2h_bytes = (double)pl->ny_local * pl->nx * 8.0;
   CUDA_TRY(cudaEventRecord(pl->ev[1], st));
   CUDA_TRY(cudaEventSynchronize(pl->ev[1]));
   rep.solve_s = elapsed_s(pl->ev[0], pl->ev[1]);
-  rep.kernel_launches = launches;
+  rep.kernel_launches = pl->launches;
   rep.status = status;
   if (rep_out) *rep_out = rep;
   return (cjm_status)status;
@@ -441,8 +483,7 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   cudaFree(p->w_dev);
   cudaFree(p->partials);
   cudaFree(p->result);
-  cudaFree(p->ctr);
-  cudaFree(p->ticket);
+  cudaFree(p->state);
   if (p->result_host) cudaFreeHost(p->result_host);
   if (p->comm) ncclCommDestroy(p->comm);
   delete p;
@@ -466,7 +507,8 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
       opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size ||
       (opt.world_size > 1 && !opt.nccl_id) ||
       (opt.method != CJM_METHOD_CHEBYSHEV && opt.method != CJM_METHOD_JACOBI) ||
-      (opt.tile_w != 0 && opt.tile_w != 128 && opt.tile_w != 256) || opt.stages < 0 ||
+      (opt.tile_w != 0 && opt.tile_w != 256 && opt.tile_w != 512) || opt.stages < 0 ||
+      opt.temporal_k < 0 || opt.temporal_k > 4 ||
       opt.stages > 32 || opt.ctas_per_sm < 0 || opt.graph_chunk < 0 || opt.max_cycles < 0 ||
       opt.jacobi_check < 0) {
     set_error("cjm_plan", "invalid argument");
@@ -528,29 +570,34 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   PLAN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
 
   // ---- launch configuration
-  pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 2;
-  if (opt.tile_w) {
-    pl->W = opt.tile_w;
-  } else {
-    // prefer 256-wide strips unless that leaves fewer than ~48 rows per CTA
-    const long long strips256 = (nx + 255) / 256;
-    const long long rows_per_cta = strips256 * nyl / ((long long)nsm * pl->ctas_per_sm);
-    pl->W = rows_per_cta >= 48 ? 256 : 128;
+  // defaults from the r01 tuning sweep on B200 (profiles/r01_v2_tune.jsonl):
+  // two sweeps fused per launch, 256-column tiles, 8-row TMA ring, 3 CTAs/SM
+  pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 3;
+  pl->NT = opt.tile_w == 512 ? 256 : 128;
+  pl->K = opt.temporal_k > 0 ? opt.temporal_k : 2;
+  if (pl->world > 1) pl->K = 1;   // deep halos for K > 1 across ranks: not implemented
+  pl->stages = opt.stages > 0 ? opt.stages : 8;
+  pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
+  int occ_min = 1 << 30;
+  const int kmax_used = pl->K;
+  for (int K = 1; K <= kmax_used; ++K) {
+    if (K != 1 && K != kmax_used) continue;
+    for (int mode = 0; mode < 3; ++mode) {
+      if (mode == MODE_RESID && K != 1) continue;
+      KernelFn k = pick_kernel(stencil, pl->NT, K, mode);
+      const size_t sm = smem_bytes(pl, K);
+      PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sm));
+      int occ = 0;
+      PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k, pl->NT + 32, sm));
+      occ_min = std::min(occ_min, occ);
+    }
   }
-  pl->stages = opt.stages > 0 ? opt.stages : (pl->W == 256 ? 8 : 12);
-  pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 256;
-  const int UROW = pl->W + 8;
-  pl->smem = (size_t)pl->stages * (UROW + pl->W) * sizeof(double) + 2 * pl->stages * sizeof(uint64_t);
-  for (int mode = 0; mode < 3; ++mode) {
-    KernelFn k = pick_kernel(stencil, pl->W, mode);
-    PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)pl->smem));
+  if (occ_min < 1) {
+    set_error("cjm_plan", "sweep kernel does not fit on an SM with these options");
+    return fail(CJM_ERR_INVALID_ARG);
   }
-  int occ = 0;
-  PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &occ, (const void*)pick_kernel(stencil, pl->W, MODE_CHECK), pl->W + 32, pl->smem));
-  if (occ < 1) return fail(CJM_ERR_INVALID_ARG);
-  pl->nctas = nsm * std::min(occ, pl->ctas_per_sm);
+  pl->nctas = nsm * std::min(occ_min, pl->ctas_per_sm);
 
   // ---- buffers: (ny_local + 2R) rows of pitch ld; interior column 0 at PADL
   pl->ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
@@ -567,10 +614,8 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
                        cudaMemcpyHostToDevice));
   PLAN_CUDA(cudaMalloc(&pl->partials, (size_t)pl->nctas * 2 * sizeof(double)));
   PLAN_CUDA(cudaMalloc(&pl->result, 2 * sizeof(double)));
-  PLAN_CUDA(cudaMalloc(&pl->ctr, sizeof(unsigned long long)));
-  PLAN_CUDA(cudaMalloc(&pl->ticket, sizeof(unsigned int)));
-  PLAN_CUDA(cudaMemset(pl->ctr, 0, sizeof(unsigned long long)));
-  PLAN_CUDA(cudaMemset(pl->ticket, 0, sizeof(unsigned int)));
+  PLAN_CUDA(cudaMalloc(&pl->state, sizeof(cjm::SweepState)));
+  PLAN_CUDA(cudaMemset(pl->state, 0, sizeof(cjm::SweepState)));
   PLAN_CUDA(cudaMallocHost(&pl->result_host, 2 * sizeof(double)));
   PLAN_CUDA(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
   for (auto& e : pl->ev) PLAN_CUDA(cudaEventCreate(&e));
@@ -624,19 +669,19 @@ cjm_status cjm_sweeps(cjm_plan_t p, const double* rhs, long long ld_rhs, double*
   cudaStream_t st = (cudaStream_t)cuda_stream;
   cjm_report rep;
   fill_static(p, &rep);
-  long long launches = 2;
+  p->launches = 0;
   STATUS_TRY(stage_in(p, rhs, ld_rhs, u, ld_u, true, cudaMemcpyDeviceToDevice, st));
-  STATUS_TRY(set_counter(p, (unsigned long long)first, st));
-  STATUS_TRY(halo_exchange(p, p->buf[first & 1], st));
+  STATUS_TRY(set_state(p, (unsigned long long)first, st));
+  STATUS_TRY(halo_exchange(p, p->buf[0], st));
   CUDA_TRY(cudaEventRecord(p->ev[2], st));
-  STATUS_TRY(run_hot(p, first, count, st, &launches));
+  STATUS_TRY(run_hot(p, count, st, &rep.hot_launches));
   CUDA_TRY(cudaEventRecord(p->ev[3], st));
-  STATUS_TRY(stage_out(p, (int)((first + count) & 1), u, ld_u, cudaMemcpyDeviceToDevice, st));
+  STATUS_TRY(stage_out(p, p->host_cur, u, ld_u, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   rep.sweep_s = elapsed_s(p->ev[2], p->ev[3]);
   rep.sweeps_timed = count;
   rep.iterations = count;
-  rep.kernel_launches = launches;
+  rep.kernel_launches = p->launches;
   if (rep_out) *rep_out = rep;
   return CJM_OK;
 }
@@ -649,12 +694,13 @@ cjm_status cjm_residual(cjm_plan_t p, const double* rhs, long long ld_rhs, const
   }
   CUDA_TRY(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  p->launches = 0;
   STATUS_TRY(stage_in(p, rhs, ld_rhs, u, ld_u, false, cudaMemcpyDeviceToDevice, st));
-  STATUS_TRY(set_counter(p, 0ull, st));
+  STATUS_TRY(set_state(p, 0ull, st));
   STATUS_TRY(halo_exchange(p, p->buf[0], st));
-  long long launches = 0;
+  STATUS_TRY(launch_sweep(p, MODE_RESID, 1, st));
   double s, m;
-  STATUS_TRY(check_sweep(p, MODE_RESID, 0, st, &s, &m, &launches));
+  STATUS_TRY(fetch_result(p, st, &s, &m));
   const double sc = std::fabs(p->gscale);
   if (l2) *l2 = std::sqrt(s) / sc;
   if (linf) *linf = m / sc;

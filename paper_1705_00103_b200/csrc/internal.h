@@ -5,9 +5,10 @@
 
 namespace cjm {
 
-// Interior column 0 of every internal row sits at column PADL: 32-byte aligned
-// stores, 16-byte aligned TMA row loads starting at column PADL - 2.
-constexpr int PADL = 4;
+// Interior column 0 of every internal row sits at column PADL: 64-byte aligned
+// rows, 16-byte aligned TMA row loads starting up to E + 2 columns to the left
+// (E <= 6: temporal blocking depth K <= 4 for r = 1 and 2).
+constexpr int PADL = 8;
 
 struct Schedule {
   double kmin = 0, kmax = 0;

@@ -27,7 +27,9 @@ def run(config, count, warm, **kw):
             plan.sweeps(bd, ud, 1, warm)
         rep = plan.sweeps(bd, ud, 1, count)
     us = 1e6 * rep["sweep_s"] / count
-    return dict(config=config, **kw, us_per_sweep=us, gbs=24.0 * nx * ny / (us * 1e-6) / 1e9)
+    K = rep["temporal_k"]
+    return dict(config=config, **kw, us_per_sweep=us, glups=nx * ny / (us * 1e-6) / 1e9,
+                gbs_per_launch=24.0 * nx * ny / (K * us * 1e-6) / 1e9)
 
 
 if __name__ == "__main__":
@@ -39,16 +41,18 @@ if __name__ == "__main__":
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--temporal-k", type=int, default=0)
+    ap.add_argument("--ks", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
     a = ap.parse_args()
     if a.tune:
         for cfgname in a.config.split(","):
-            for tw, stg, cps in itertools.product((128, 256), (4, 8, 12, 16), (1, 2, 3, 4)):
+            for K, tw, stg, cps in itertools.product(a.ks, (256, 512), (4, 8, 12), (1, 2, 3, 4)):
                 try:
-                    print(json.dumps(run(cfgname, 2000, 200, tile_w=tw, stages=stg, ctas_per_sm=cps)),
-                          flush=True)
+                    print(json.dumps(run(cfgname, 2400, 240, tile_w=tw, stages=stg, ctas_per_sm=cps,
+                                         temporal_k=K)), flush=True)
                 except Exception as e:  # noqa: BLE001
                     print(json.dumps(dict(config=cfgname, tile_w=tw, stages=stg, ctas_per_sm=cps,
-                                          error=str(e))), flush=True)
+                                          temporal_k=K, error=str(e))), flush=True)
     else:
         print(json.dumps(run(a.config, a.count, a.warm, tile_w=a.tile_w, stages=a.stages,
-                             ctas_per_sm=a.ctas_per_sm)))
+                             ctas_per_sm=a.ctas_per_sm, temporal_k=a.temporal_k)))

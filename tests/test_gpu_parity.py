@@ -56,7 +56,7 @@ SHAPES = [(8, 8), (64, 64), (100, 37), (257, 300), (513, 70), (1000, 11), (4, 4)
 
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("nx,ny", SHAPES)
-@pytest.mark.parametrize("tile_w", (128, 256))
+@pytest.mark.parametrize("tile_w", (256, 512))
 def test_one_sweep_bitwise(stencil, nx, ny, tile_w):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=inputs.SEED_BASE + nx + 7 * ny)
@@ -72,13 +72,16 @@ def test_one_sweep_bitwise(stencil, nx, ny, tile_w):
 
 
 @pytest.mark.parametrize("stencil", (5, 9, 17))
-@pytest.mark.parametrize("nx,ny,count", [(300, 257, 37), (1030, 515, 20), (64, 64, 324)])
-def test_sweep_segment_bitwise(stencil, nx, ny, count):
+@pytest.mark.parametrize("nx,ny,count", [(300, 257, 37), (1030, 515, 20), (64, 64, 324),
+                                         (9, 700, 13), (520, 6, 11)])
+@pytest.mark.parametrize("temporal_k", (1, 2, 3, 4))
+def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k):
     """A run of sweeps through the CUDA-graph hot loop (spans several graph
-    chunks when count > graph_chunk) vs the oracle sweep by sweep."""
+    chunks when count > graph_chunk), K sweeps fused per launch (temporal
+    blocking), vs the oracle sweep by sweep."""
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=3)
-    with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=16) as plan:
+    with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=4, temporal_k=temporal_k) as plan:
         w = plan.info()["weights"]
         ud = dev(u0)
         plan.sweeps(dev(b), ud, 5, count)
@@ -89,9 +92,11 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count):
         assert_field_parity(host(ud), u, r)
 
 
-@pytest.mark.parametrize("cfg", [dict(tile_w=128, stages=4, ctas_per_sm=1),
-                                 dict(tile_w=256, stages=16, ctas_per_sm=3),
-                                 dict(tile_w=128, stages=32, ctas_per_sm=2, graph_chunk=7)])
+@pytest.mark.parametrize("cfg", [dict(tile_w=256, stages=4, ctas_per_sm=1),
+                                 dict(tile_w=512, stages=16, ctas_per_sm=3),
+                                 dict(tile_w=256, stages=32, ctas_per_sm=2, graph_chunk=7),
+                                 dict(tile_w=512, temporal_k=3, stages=6),
+                                 dict(tile_w=256, temporal_k=4, ctas_per_sm=4)])
 def test_launch_configuration_does_not_change_result(cfg):
     nx, ny = 777, 301
     u0, b, h = inputs.test_problem(nx, ny, 1, init="random", seed=5)
@@ -106,7 +111,7 @@ def test_launch_configuration_does_not_change_result(cfg):
 
 # ------------------------------------------------------------ residual
 @pytest.mark.parametrize("stencil", (5, 9, 17))
-def test_residual_matches_oracle(stencil):
+def test_residual_matches_oracle(stencil):  # noqa: D103
     r = oracle.reach(stencil)
     nx, ny = 333, 129
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=8)
@@ -120,11 +125,12 @@ def test_residual_matches_oracle(stencil):
 # ------------------------------------------------------------ full solves
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("n,init", [(64, "zero"), (64, "random"), (200, "zero"), (129, "random")])
-def test_solve_matches_oracle(stencil, n, init):
+@pytest.mark.parametrize("temporal_k", (1, 2, 4))
+def test_solve_matches_oracle(stencil, n, init, temporal_k):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(n, n, r, init=init)
     uo, ro = oracle.solve(stencil, h, 1e-8, b, u0)
-    with cjm.Plan(stencil, n, n, h, 1e-8) as plan:
+    with cjm.Plan(stencil, n, n, h, 1e-8, temporal_k=temporal_k) as plan:
         ud = dev(u0)
         rep = plan.solve(dev(b), ud)
     assert rep["status"] == "CJM_OK" and ro["status"] == "OK"
@@ -134,11 +140,12 @@ def test_solve_matches_oracle(stencil, n, init):
     assert_field_parity(host(ud), uo, r)
 
 
-def test_solve_nonsquare_ragged():
+@pytest.mark.parametrize("temporal_k", (1, 3))
+def test_solve_nonsquare_ragged(temporal_k):
     nx, ny = 301, 157
     u0, b, h = inputs.test_problem(nx, ny, 2)
     uo, ro = oracle.solve(17, h, 1e-8, b, u0)
-    with cjm.Plan(17, nx, ny, h, 1e-8) as plan:
+    with cjm.Plan(17, nx, ny, h, 1e-8, temporal_k=temporal_k) as plan:
         ud = dev(u0)
         rep = plan.solve(dev(b), ud)
     assert rep["iterations"] == ro["iterations"]
@@ -193,14 +200,18 @@ def test_jacobi_method_matches_oracle_sweeps():
 
 
 def test_bad_pitch_is_invalid_arg():
+    import ctypes as C
     u0, b, h = inputs.test_problem(64, 64, 1)
     with cjm.Plan(9, 64, 64, h, 1e-8) as plan:
-        narrow = torch.zeros(66, 60, dtype=torch.float64, device="cuda")   # pitch 60 < nx + 2r
-        with pytest.raises(cjm.CJMError) as e:
-            plan.solve(dev(b), narrow)
-        assert e.value.name == "CJM_ERR_INVALID_ARG"
+        ud, bd = dev(u0), dev(b)
+        # pitch 60 < nx + 2r: rejected by the C ABI itself
+        st = cjm.lib().cjm_solve(plan._h, C.c_void_p(bd.data_ptr()), 64, C.c_void_p(ud.data_ptr()), 60,
+                                 C.c_void_p(torch.cuda.current_stream().cuda_stream), None)
+        assert cjm.STATUS[st] == "CJM_ERR_INVALID_ARG"
+        st = cjm.lib().cjm_solve(plan._h, None, 64, C.c_void_p(ud.data_ptr()), 66, None, None)
+        assert cjm.STATUS[st] == "CJM_ERR_INVALID_ARG"
         with pytest.raises(ValueError):       # shape checked by the binding
-            plan.solve(dev(b), dev(u0)[:, :60])
+            plan.solve(bd, ud[:, :60])
 
 
 # ------------------------------------------------------------ stored oracle solves
@@ -212,7 +223,8 @@ def _digest_cases():
 
 
 @pytest.mark.parametrize("name", _digest_cases())
-def test_solve_matches_stored_oracle_digest(name):
+@pytest.mark.parametrize("temporal_k", (1, 2))
+def test_solve_matches_stored_oracle_digest(name, temporal_k):
     """Full solves at BASELINE sizes vs the oracle's stored result
     (tests/make_oracle_digests.py): same iterations, sampled nodes within
     1e-10 max|u| and bitwise, and the SHA-256 of the whole interior."""
@@ -225,7 +237,7 @@ def test_solve_matches_stored_oracle_digest(name):
     r = oracle.reach(st)
     u0, b, h2 = inputs.test_problem(nx, ny, r, init=rec["init"])
     assert h2 == h
-    with cjm.Plan(st, nx, ny, h, tol) as plan:
+    with cjm.Plan(st, nx, ny, h, tol, temporal_k=temporal_k) as plan:
         ud = dev(u0)
         rep = plan.solve(dev(b), ud)
     assert rep["status"] == "CJM_OK"
