@@ -280,11 +280,14 @@ def main():
     iters = reps[-1]["iterations"]
     lups_total = float(nx) * ny * sum(r["iterations"] for r in reps)
     value = lups_total / t_dev / 1e9
-    # dominant kernel: the hot sweep, timed with CUDA events on its launching stream
+    # dominant kernel: the hot sweep kernel (K fused sweeps per launch), timed
+    # with CUDA events on its launching stream around the graph launches
     sweep_s = sum(r["sweep_s"] for r in reps)
-    sweeps = sum(r["sweeps_timed"] for r in reps)
-    t_sweep = sweep_s / max(sweeps, 1)
-    achieved = BYTES_PER_LUP * float(nx) * nyl / t_sweep / 1e9
+    hot = sum(r["hot_launches"] for r in reps)
+    K = reps[-1]["temporal_k"]
+    t_launch = sweep_s / max(hot, 1)
+    bytes_per_launch = BYTES_PER_LUP * float(nx) * nyl      # read u, read g, write u' once per launch
+    achieved = bytes_per_launch / t_launch / 1e9
     peak, peak_kind = measured_peaks()
     traffic = ncu_traffic(args.config) if world == 1 else None
     launches = int(sum(r["kernel_launches"] for r in reps))
@@ -323,9 +326,14 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                         "kernel": f"cjm_sweep_kernel<{stencil}>",
-                         "algorithmic_bytes_per_launch": BYTES_PER_LUP * nx * nyl,
-                         "avg_launch_us": 1e6 * t_sweep},
+                         "kernel": f"cjm_sweep_kernel<{stencil},K={K}>",
+                         "sweeps_per_launch": K,
+                         "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "avg_launch_us": 1e6 * t_launch,
+                         "sweep_glups": K * float(nx) * nyl / t_launch / 1e9},
+            "breakdown_ms": {"plan": 1e3 * statistics.mean(r["plan_s"] for r in reps),
+                             "solve_device": 1e3 * statistics.mean(r["solve_s"] for r in reps),
+                             "hot_sweeps": 1e3 * statistics.mean(r["sweep_s"] for r in reps)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -202,8 +202,15 @@ cjm_status cjm_get_nccl_id(void *out128);
  * world_size owns interior rows [floor(g ny / W), floor((g+1) ny / W)). */
 cjm_status cjm_slab(int ny, int world_size, int rank, int *y0, int *ny_local);
 
-/* Free every device buffer, graph and communicator of the plan. NULL is ok. */
+/* Release every device buffer, graph and communicator of the plan.  NULL is
+ * ok.  The field-sized buffers go to the library's device-buffer cache
+ * (reused by the next plan of the same size); cjm_pool_trim frees them. */
 cjm_status cjm_plan_destroy(cjm_plan_t p);
+
+/* Return every cached device buffer to the driver (cudaFree).  Call when no
+ * plan is being created concurrently.  cached_bytes_before (nullable)
+ * receives the bytes that were cached. */
+cjm_status cjm_pool_trim(long long *cached_bytes_before);
 
 const char *cjm_status_str(int status);
 const char *cjm_last_error(void);

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcjm.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("cjm.cu", "schedule.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("cjm.cu", "schedule.cpp", "pool.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("sweep.cuh", "internal.h")] + \
     [os.path.join(ROOT, "include", "cjm.h")]
 

@@ -31,7 +31,7 @@ STATUS = {0: "CJM_OK", 1: "CJM_ERR_INVALID_ARG", 2: "CJM_ERR_UNSUPPORTED",
 # Symbols include/cjm.h declares (tests/test_abi.py checks the header agrees).
 EXPORTS = ("cjm_default_options", "cjm_schedule", "cjm_plan", "cjm_plan_info", "cjm_solve",
            "cjm_solve_host", "cjm_sweeps", "cjm_residual", "cjm_get_nccl_id", "cjm_slab",
-           "cjm_plan_destroy", "cjm_status_str", "cjm_last_error", "cjm_version")
+           "cjm_plan_destroy", "cjm_pool_trim", "cjm_status_str", "cjm_last_error", "cjm_version")
 
 
 class CJMError(RuntimeError):
@@ -92,6 +92,7 @@ def lib():
     L.cjm_get_nccl_id.argtypes = [vp]
     L.cjm_slab.argtypes = [i, i, i, C.POINTER(i), C.POINTER(i)]
     L.cjm_plan_destroy.argtypes = [vp]
+    L.cjm_pool_trim.argtypes = [C.POINTER(ll)]
     L.cjm_status_str.argtypes = [i]
     L.cjm_status_str.restype = C.c_char_p
     L.cjm_last_error.restype = C.c_char_p
@@ -288,6 +289,13 @@ def cjm_residual(plan: Plan, rhs, u, stream=None):
 
 def cjm_plan_destroy(plan: Plan) -> None:
     plan.close()
+
+
+def cjm_pool_trim() -> int:
+    """Free the library's cached device buffers; returns the bytes released."""
+    b = C.c_longlong()
+    _check(lib().cjm_pool_trim(C.byref(b)), "cjm_pool_trim")
+    return b.value
 
 
 def cjm_version() -> int:

@@ -141,7 +141,8 @@ namespace {
 size_t smem_bytes(const cjm_plan_s* pl, int K) {
   const int T = 2 * pl->NT, ROW = T + 8;
   return (size_t)pl->stages * (ROW + T) * sizeof(double) +
-         (size_t)(K - 1) * 2 * ROW * sizeof(double) + 2 * (size_t)pl->stages * sizeof(uint64_t);
+         (size_t)(K - 1) * (2 * pl->R + 1) * ROW * sizeof(double) +
+         2 * (size_t)pl->stages * sizeof(uint64_t);
 }
 
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur.
@@ -477,9 +478,9 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   p->graphs.clear();
   for (auto& e : p->ev) if (e) cudaEventDestroy(e);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
-  cudaFree(p->buf[0]);
-  cudaFree(p->buf[1]);
-  cudaFree(p->G);
+  cjm::pool_free(p->device, p->buf_elems * sizeof(double), p->buf[0]);
+  cjm::pool_free(p->device, p->buf_elems * sizeof(double), p->buf[1]);
+  cjm::pool_free(p->device, p->g_elems * sizeof(double), p->G);
   cudaFree(p->w_dev);
   cudaFree(p->partials);
   cudaFree(p->result);
@@ -570,27 +571,31 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   PLAN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
 
   // ---- launch configuration
-  // defaults from the r01 tuning sweep on B200 (profiles/r01_v2_tune.jsonl):
-  // two sweeps fused per launch, 256-column tiles, 8-row TMA ring, 3 CTAs/SM
-  pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 3;
+  // defaults from the r01 tuning sweep on B200 (profiles/r01_v3b_tune.jsonl):
+  // two sweeps fused per launch, 256-column tiles, 4-row TMA ring, 4 CTAs/SM
+  pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 4;
   pl->NT = opt.tile_w == 512 ? 256 : 128;
   pl->K = opt.temporal_k > 0 ? opt.temporal_k : 2;
   if (pl->world > 1) pl->K = 1;   // deep halos for K > 1 across ranks: not implemented
-  pl->stages = opt.stages > 0 ? opt.stages : 8;
+  pl->stages = opt.stages > 0 ? opt.stages : 4;
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
+  // The grid is sized for the hot kernel (persistent: ctas_per_sm per SM, all
+  // resident).  Check / residual / remainder kernels may need more registers;
+  // they then run the same grid in more than one wave, which is correct
+  // because no CTA ever waits for another.
   int occ_min = 1 << 30;
-  const int kmax_used = pl->K;
-  for (int K = 1; K <= kmax_used; ++K) {
-    if (K != 1 && K != kmax_used) continue;
+  for (int K = 1; K <= pl->K; ++K) {
+    if (K != 1 && K != pl->K) continue;
     for (int mode = 0; mode < 3; ++mode) {
       if (mode == MODE_RESID && K != 1) continue;
       KernelFn k = pick_kernel(stencil, pl->NT, K, mode);
       const size_t sm = smem_bytes(pl, K);
       PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sm));
-      int occ = 0;
-      PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k, pl->NT + 32, sm));
-      occ_min = std::min(occ_min, occ);
+      if (K == pl->K && mode == MODE_HOT) {
+        PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_min, (const void*)k,
+                                                                pl->NT + 32, sm));
+      }
     }
   }
   if (occ_min < 1) {
@@ -603,9 +608,9 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   pl->ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
   pl->buf_elems = (size_t)(nyl + 2 * R) * pl->ld;
   pl->g_elems = (size_t)nyl * pl->ld;
-  PLAN_CUDA(cudaMalloc(&pl->buf[0], pl->buf_elems * sizeof(double)));
-  PLAN_CUDA(cudaMalloc(&pl->buf[1], pl->buf_elems * sizeof(double)));
-  PLAN_CUDA(cudaMalloc(&pl->G, pl->g_elems * sizeof(double)));
+  PLAN_CUDA(cjm::pool_alloc(dev, pl->buf_elems * sizeof(double), (void**)&pl->buf[0]));
+  PLAN_CUDA(cjm::pool_alloc(dev, pl->buf_elems * sizeof(double), (void**)&pl->buf[1]));
+  PLAN_CUDA(cjm::pool_alloc(dev, pl->g_elems * sizeof(double), (void**)&pl->G));
   PLAN_CUDA(cudaMemset(pl->buf[0], 0, pl->buf_elems * sizeof(double)));
   PLAN_CUDA(cudaMemset(pl->buf[1], 0, pl->buf_elems * sizeof(double)));
   PLAN_CUDA(cudaMemset(pl->G, 0, pl->g_elems * sizeof(double)));
@@ -723,6 +728,12 @@ const char* cjm_status_str(int s) {
 }
 
 const char* cjm_last_error(void) { return g_last_error.c_str(); }
+
+cjm_status cjm_pool_trim(long long* cached_bytes_before) {
+  if (cached_bytes_before) *cached_bytes_before = (long long)cjm::pool_cached_bytes();
+  cjm::pool_trim();
+  return CJM_OK;
+}
 
 int cjm_version(void) { return 100 * CJM_VERSION_MAJOR + CJM_VERSION_MINOR; }
 

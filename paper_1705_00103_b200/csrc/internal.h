@@ -1,7 +1,10 @@
 // Internal declarations of libcjm (not part of the C ABI).
 #pragma once
 
+#include <cstddef>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 namespace cjm {
 
@@ -23,5 +26,11 @@ long long chebyshev_degree(double kmin, double kmax, double tol);
 long long smooth_cycle_length(long long m, int* a_out, int* b_out);
 std::vector<long long> lebedev23_order(int a, int b);
 bool build_schedule(int stencil, int nx, int ny, double tol, int order, Schedule* s);
+
+// device-buffer cache (pool.cpp)
+cudaError_t pool_alloc(int device, size_t bytes, void** out);
+void pool_free(int device, size_t bytes, void* p);
+void pool_trim();
+size_t pool_cached_bytes();
 
 }  // namespace cjm

@@ -97,6 +97,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0,
 // both addresses 16-byte aligned).  Streaming data: L2 evict-first policy.
 __device__ __forceinline__ void tma_row_load(void* dst, const void* src, uint32_t bytes,
@@ -128,6 +143,11 @@ __device__ __forceinline__ double nan_max(double a, double b) {
 // The fixed association of DESIGN R6; __dadd_rn / __fma_rn forbid any other
 // contraction.  Window index R is the output row; uc = centre values, h1 =
 // horizontal pair sums at distance 1 (uW + uE), h2 at distance 2.
+// The a_k = -c_k/c_C live in the constant bank so DFMA reads them directly
+// (the same doubles as the literals of DESIGN R6).
+__constant__ double c_coef[7] = {0.25, 0.2, 0.05, 64.0 / 300.0, -4.0 / 300.0, 16.0 / 300.0,
+                                 -1.0 / 300.0};
+
 template <int STENCIL>
 struct Point;
 
@@ -137,7 +157,7 @@ struct Point<5> {
   __device__ static __forceinline__ double jacobi_target(const double* uc, const double* h1,
                                                         const double*, double g) {
     const double S1 = __dadd_rn(h1[1], __dadd_rn(uc[0], uc[2]));
-    return __fma_rn(0.25, S1, g);
+    return __fma_rn(c_coef[0], S1, g);
   }
 };
 
@@ -148,7 +168,7 @@ struct Point<9> {
                                                         const double*, double g) {
     const double S1 = __dadd_rn(h1[1], __dadd_rn(uc[0], uc[2]));
     const double S2 = __dadd_rn(h1[0], h1[2]);
-    return __fma_rn(0.2, S1, __fma_rn(0.05, S2, g));
+    return __fma_rn(c_coef[1], S1, __fma_rn(c_coef[2], S2, g));
   }
 };
 
@@ -161,10 +181,10 @@ struct Point<17> {
     const double S2 = __dadd_rn(h2[2], __dadd_rn(uc[0], uc[4]));
     const double S3 = __dadd_rn(h1[1], h1[3]);
     const double S4 = __dadd_rn(h2[0], h2[4]);
-    return __fma_rn(64.0 / 300.0, S1,
-           __fma_rn(-4.0 / 300.0, S2,
-           __fma_rn(16.0 / 300.0, S3,
-           __fma_rn(-1.0 / 300.0, S4, g))));
+    return __fma_rn(c_coef[3], S1,
+           __fma_rn(c_coef[4], S2,
+           __fma_rn(c_coef[5], S3,
+           __fma_rn(c_coef[6], S4, g))));
   }
 };
 
@@ -237,6 +257,161 @@ struct TileGeom {
   static constexpr int E = (K == 1) ? 0 : ((R * (K - 1) + 1) & ~1);
 };
 
+
+// Register state of one consumer thread, carried across the segments of a CTA.
+template <int R, int K>
+struct ConsumerState {
+  static constexpr int P = 2 * R + 1;
+  // level l (0-based; applies sweep n+l): the last P rows of level l-1 values
+  // (level 0: the input iterate) for the thread's columns a, b, in a ring of
+  // P slots (the row pushed at step kk sits in slot kk mod P), and the g of
+  // level l-1 pushed at step kk (used R+1 steps later by level l)
+  double ua[K][P], ub[K][P], h1a[K][P], h1b[K][P], h2a[K][P], h2b[K][P];
+  double gra[K][P], grb[K][P];
+  double wl[K];
+  int stage;
+  uint32_t phase;
+  uint32_t full_a, empty_a;   // shared addresses of the mbarrier arrays
+  __device__ __forceinline__ void init(const SweepParams& p, unsigned long long n, uint64_t* full,
+                                       uint64_t* empty) {
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+      wl[l] = __ldg(p.w + (long long)((n + l) % (unsigned long long)p.P));
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        ua[l][q] = ub[l][q] = h1a[l][q] = h1b[l][q] = h2a[l][q] = h2b[l][q] = 0.0;
+        gra[l][q] = grb[l][q] = 0.0;
+      }
+    }
+    stage = 0;
+    phase = 0;
+    full_a = smem_addr(full);
+    empty_a = smem_addr(empty);
+  }
+};
+
+// One segment (rows [ja, jb) of the strip whose tile starts at column c0) of
+// the consumer loop.  The step loop is unrolled by P = 2R+1 so every ring
+// slot index is a compile-time constant (no register moves for the sliding
+// windows).  Levels are skewed by one step each: level l reads the line
+// level l-1 wrote at the previous step, so one named barrier per step serves
+// all levels.
+template <int STENCIL, int NT, int K, bool REDUCE, bool STORE, bool FAST>
+__device__ __forceinline__ void consumer_segment(ConsumerState<Point<STENCIL>::R, K>& cs,
+                                                 const SweepParams& p, const double* su,
+                                                 const double* sg, double* lb, double* dst,
+                                                 int ja, int jb, int c0, int tid, int lane,
+                                                 double& acc_s, double& acc_m) {
+  constexpr int R = Point<STENCIL>::R;
+  constexpr int P = 2 * R + 1;
+  constexpr int T = 2 * NT;
+  constexpr int E = TileGeom<R, K>::E;
+  constexpr int ROW = T + 8;
+  const long long ld = p.ld;
+  const int rows = p.rows;
+      const int ca = c0 + 2 * tid, cb = ca + 1;
+      const bool ina = ca >= 0 && ca < p.nx, inb = cb >= 0 && cb < p.nx;
+      const bool owna = ina && ca >= c0 + E && ca < c0 + T - E;
+      const bool ownb = inb && cb >= c0 + E && cb < c0 + T - E;
+      const int nin = jb - ja + 2 * K * R;
+      const int nsteps = nin + K - 1;
+      const int row_base = ja - K * R;               // global row of input step 0
+      double* outp = dst + (long long)(ja + R) * ld + PADL + ca;
+      for (int k0 = 0; k0 < nsteps; k0 += P) {
+#pragma unroll
+        for (int ph = 0; ph < P; ++ph) {
+          const int kk = k0 + ph;
+          if (kk < nsteps) {
+            // ---- level 0 input: the TMA row of step kk (slot ph)
+            double g0a = 0.0, g0b = 0.0;
+            if (kk < nin) {
+              mbar_wait_a(cs.full_a + 8u * cs.stage, cs.phase);
+              double c_a, c_b, l2, l1, r1, r2;
+              read_row<R>(su + (size_t)cs.stage * ROW, tid, c_a, c_b, l2, l1, r1, r2);
+              if (kk >= 2 * R) {
+                const double2 gv = *reinterpret_cast<const double2*>(sg + (size_t)cs.stage * T + 2 * tid);
+                g0a = gv.x;
+                g0b = gv.y;
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive_a(cs.empty_a + 8u * cs.stage);
+              if (++cs.stage == p.stages) { cs.stage = 0; cs.phase ^= 1u; }
+              cs.ua[0][ph] = c_a;
+              cs.ub[0][ph] = c_b;
+              cs.h1a[0][ph] = __dadd_rn(l1, c_b);      // u(a-1) + u(a+1)
+              cs.h1b[0][ph] = __dadd_rn(c_a, r1);      // u(b-1) + u(b+1)
+              if (R == 2) {
+                cs.h2a[0][ph] = __dadd_rn(l2, r1);     // u(a-2) + u(a+2)
+                cs.h2b[0][ph] = __dadd_rn(l1, r2);     // u(b-2) + u(b+2)
+              }
+            }
+            // ---- levels 1..K-1 input: level l-1's line of step kk-1
+#pragma unroll
+            for (int l = 1; l < K; ++l) {
+              const int lo = 2 * l * R + l - 1;     // first active step of level l-1
+              if (kk - 1 >= lo && kk - 1 < nin + l - 1) {
+                const double* row = lb + (size_t)((l - 1) * P + (ph + P - 1) % P) * ROW;
+                double l2, l1, r1, r2;
+                read_nbrs<R>(row, tid, l2, l1, r1, r2);
+                const double2 c = *reinterpret_cast<const double2*>(row + 2 * tid + 2);
+                cs.ua[l][ph] = c.x;
+                cs.ub[l][ph] = c.y;
+                cs.h1a[l][ph] = __dadd_rn(l1, c.y);
+                cs.h1b[l][ph] = __dadd_rn(c.x, r1);
+                if (R == 2) {
+                  cs.h2a[l][ph] = __dadd_rn(l2, r1);
+                  cs.h2b[l][ph] = __dadd_rn(l1, r2);
+                }
+              }
+            }
+            // ---- compute every active level
+#pragma unroll
+            for (int l = 0; l < K; ++l) {
+              const double ga = (l == 0) ? g0a : cs.gra[l][(ph + P - R - 1) % P];
+              const double gb = (l == 0) ? g0b : cs.grb[l][(ph + P - R - 1) % P];
+              if (l + 1 < K) { cs.gra[l + 1][ph] = ga; cs.grb[l + 1][ph] = gb; }
+              const int first = 2 * (l + 1) * R + l;   // first active step of level l
+              if (kk >= first && kk < nin + l) {
+                double wa[P], wb[P], xa[P], xb[P], ya[P], yb[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) {          // logical row q -> slot (ph+1+q) mod P
+                  const int sl = (ph + 1 + q) % P;
+                  wa[q] = cs.ua[l][sl]; wb[q] = cs.ub[l][sl];
+                  xa[q] = cs.h1a[l][sl]; xb[q] = cs.h1b[l][sl];
+                  ya[q] = cs.h2a[l][sl]; yb[q] = cs.h2b[l][sl];
+                }
+                const int G = row_base + kk - (l + 1) * R - l;   // global row of the output
+                const bool rowin = (unsigned)G < (unsigned)rows;
+                const double Ja = Point<STENCIL>::jacobi_target(wa, xa, ya, ga);
+                const double Jb = Point<STENCIL>::jacobi_target(wb, xb, yb, gb);
+                const double da = __dsub_rn(Ja, wa[R]);
+                const double db = __dsub_rn(Jb, wb[R]);
+                const double oa = (FAST || (rowin && ina)) ? __fma_rn(cs.wl[l], da, wa[R]) : wa[R];
+                const double ob = (FAST || (rowin && inb)) ? __fma_rn(cs.wl[l], db, wb[R]) : wb[R];
+                if (REDUCE && l == 0 && (unsigned)(G - ja) < (unsigned)(jb - ja)) {
+                  if (owna) { acc_s = __fma_rn(da, da, acc_s); acc_m = nan_max(acc_m, fabs(da)); }
+                  if (ownb) { acc_s = __fma_rn(db, db, acc_s); acc_m = nan_max(acc_m, fabs(db)); }
+                }
+                if (l < K - 1) {
+                  double* row = lb + (size_t)(l * P + ph) * ROW;
+                  *reinterpret_cast<double2*>(row + 2 * tid + 2) = make_double2(oa, ob);
+                } else {
+                  if (STORE) {
+                    if (FAST ? (tid >= E / 2 && tid < NT - E / 2) : (owna && ownb))
+                      *reinterpret_cast<double2*>(outp) = make_double2(oa, ob);
+                    else if (owna) outp[0] = oa;
+                    else if (ownb) outp[1] = ob;
+                  }
+                  outp += ld;
+                }
+              }
+            }
+            if (K > 1) consumer_bar(NT);
+          }
+        }
+      }
+}
+
 // ------------------------------------------------------------------- kernel
 template <int STENCIL, int NT, int K, bool REDUCE, bool STORE>
 __global__ void __launch_bounds__(NT + 32)
@@ -251,8 +426,8 @@ cjm_sweep_kernel(const SweepParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* su = reinterpret_cast<double*>(smem_raw);
   double* sg = su + (size_t)p.stages * ROW;
-  double* lb = sg + (size_t)p.stages * T;                       // (K-1) x 2 rows
-  uint64_t* full = reinterpret_cast<uint64_t*>(lb + (size_t)(K - 1) * 2 * ROW);
+  double* lb = sg + (size_t)p.stages * T;                       // (K-1) x (2R+1) rows
+  uint64_t* full = reinterpret_cast<uint64_t*>(lb + (size_t)(K - 1) * (2 * R + 1) * ROW);
   uint64_t* empty = full + p.stages;
   __shared__ double red_s[NWARP], red_m[NWARP];
   __shared__ int is_last;
@@ -268,7 +443,7 @@ cjm_sweep_kernel(const SweepParams p) {
     fence_mbar_init();
   }
   if (K > 1)
-    for (int e = tid; e < (K - 1) * 2 * ROW; e += blockDim.x) lb[e] = 0.0;
+    for (int e = tid; e < (K - 1) * (2 * R + 1) * ROW; e += blockDim.x) lb[e] = 0.0;
   __syncthreads();
 
   const unsigned long long n = __ldcg(&p.state->n);
@@ -325,109 +500,23 @@ cjm_sweep_kernel(const SweepParams p) {
     }
   } else {
     // ---------------------------------------------- consumer threads (NT)
-    double wl[K];
-#pragma unroll
-    for (int l = 0; l < K; ++l) wl[l] = __ldg(p.w + (long long)((n + l) % (unsigned long long)p.P));
-    int stage = 0;
-    uint32_t phase = 0;
-    Window<R> win[K];
-    double gf[K][R + 1][2];   // g handed from level l-1 to level l, delayed R+1 steps
+    ConsumerState<R, K> cs;
+    cs.init(p, n, full, empty);
     for (long long uu = u_begin; uu < u_end;) {
       const int strip = (int)(uu / rows);
       const int ja = (int)(uu - (long long)strip * rows);
       const long long seg_end = min(u_end, (long long)(strip + 1) * rows);
       const int jb = ja + (int)(seg_end - uu);
       const int c0 = strip * TOUT - E;
-      const int ca = c0 + 2 * tid, cb = ca + 1;
-      const bool ina = ca >= 0 && ca < p.nx, inb = cb >= 0 && cb < p.nx;
-      const bool owna = ina && ca >= c0 + E && ca < c0 + T - E;
-      const bool ownb = inb && cb >= c0 + E && cb < c0 + T - E;
-      const int nin = jb - ja + 2 * K * R;
-      const int nsteps = nin + K - 1;
-#pragma unroll
-      for (int l = 0; l < K; ++l) {
-        win[l].clear();
-#pragma unroll
-        for (int q = 0; q <= R; ++q) { gf[l][q][0] = 0.0; gf[l][q][1] = 0.0; }
-      }
-      for (int k = 0; k < nsteps; ++k) {
-        // ---- level 1 input: the TMA row
-        double g1a = 0.0, g1b = 0.0;
-        if (k < nin) {
-          mbar_wait(&full[stage], phase);
-          double ca_, cb_, l2, l1, r1, r2;
-          read_row<R>(su + (size_t)stage * ROW, tid, ca_, cb_, l2, l1, r1, r2);
-          if (k >= 2 * R) {
-            const double2 gv = *reinterpret_cast<const double2*>(sg + (size_t)stage * T + 2 * tid);
-            g1a = gv.x; g1b = gv.y;
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
-          if (++stage == p.stages) { stage = 0; phase ^= 1u; }
-          win[0].push(ca_, cb_, l2, l1, r1, r2);
-        }
-        // ---- levels 2..K input: previous step's output line of level l-1
-#pragma unroll
-        for (int l = 1; l < K; ++l) {
-          // level l-1 (0-based) produced a row at step k-1 ?
-          const int lo = 2 * l * R + l - 1;        // first active step of level l-1 (0-based l-1)
-          if (k - 1 >= lo && k - 1 < nin + l - 1) {
-            const double* row = lb + (size_t)((l - 1) * 2 + ((k - 1) & 1)) * ROW;
-            double l2, l1, r1, r2;
-            read_nbrs<R>(row, tid, l2, l1, r1, r2);
-            // own centre values: what this thread wrote at step k-1
-            const double2 c = *reinterpret_cast<const double2*>(row + 2 * tid + 2);
-            win[l].push(c.x, c.y, l2, l1, r1, r2);
-          }
-        }
-        // ---- compute every active level
-        double gcur[K][2];
-#pragma unroll
-        for (int l = 0; l < K; ++l) {
-          // g of this level's row: level 0 from the TMA slot, level l from the
-          // FIFO fed by level l-1 (R+1 steps earlier)
-          const double ga = (l == 0) ? g1a : gf[l][R][0];
-          const double gb = (l == 0) ? g1b : gf[l][R][1];
-          gcur[l][0] = ga;
-          gcur[l][1] = gb;
-          const int first = 2 * (l + 1) * R + l;   // first active step of level l (0-based)
-          if (k >= first && k < nin + l) {
-            const int q = k - (l + 1) * R - l;      // segment row index of the output
-            const int G = ja - K * R + q;           // global row
-            const bool rowin = G >= 0 && G < rows;
-            const Window<R>& wv = win[l];
-            const double Ja = Point<STENCIL>::jacobi_target(wv.ua, wv.h1a, wv.h2a, ga);
-            const double Jb = Point<STENCIL>::jacobi_target(wv.ub, wv.h1b, wv.h2b, gb);
-            const double da = __dsub_rn(Ja, wv.ua[R]);
-            const double db = __dsub_rn(Jb, wv.ub[R]);
-            const double oa = (rowin && ina) ? __fma_rn(wl[l], da, wv.ua[R]) : wv.ua[R];
-            const double ob = (rowin && inb) ? __fma_rn(wl[l], db, wv.ub[R]) : wv.ub[R];
-            if (REDUCE && l == 0 && G >= ja && G < jb) {
-              if (owna) { acc_s = __fma_rn(da, da, acc_s); acc_m = nan_max(acc_m, fabs(da)); }
-              if (ownb) { acc_s = __fma_rn(db, db, acc_s); acc_m = nan_max(acc_m, fabs(db)); }
-            }
-            if (l < K - 1) {
-              double* row = lb + (size_t)(l * 2 + (k & 1)) * ROW;
-              *reinterpret_cast<double2*>(row + 2 * tid + 2) = make_double2(oa, ob);
-            } else if (STORE) {
-              double* o = dst + (long long)(G + R) * ld + PADL + ca;
-              if (owna && ownb) *reinterpret_cast<double2*>(o) = make_double2(oa, ob);
-              else if (owna) o[0] = oa;
-              else if (ownb) o[1] = ob;
-            }
-          }
-        }
-        // feed the g FIFOs (every step, so FIFO positions count steps):
-        // level l reads gf[l][R] = level l-1's g from step k-1-R
-#pragma unroll
-        for (int l = 1; l < K; ++l) {
-#pragma unroll
-          for (int q = R; q > 0; --q) { gf[l][q][0] = gf[l][q - 1][0]; gf[l][q][1] = gf[l][q - 1][1]; }
-          gf[l][0][0] = gcur[l - 1][0];
-          gf[l][0][1] = gcur[l - 1][1];
-        }
-        if (K > 1) consumer_bar(NT);
-      }
+      // FAST: every row the segment touches is interior and the tile holds no
+      // ghost / padding column, so no node of it is pass-through
+      const bool fast = ja - K * R >= 0 && jb + K * R <= rows && c0 >= 0 && c0 + T <= p.nx;
+      if (fast)
+        consumer_segment<STENCIL, NT, K, REDUCE, STORE, true>(cs, p, su, sg, lb, dst, ja, jb, c0,
+                                                               tid, lane, acc_s, acc_m);
+      else
+        consumer_segment<STENCIL, NT, K, REDUCE, STORE, false>(cs, p, su, sg, lb, dst, ja, jb, c0,
+                                                                tid, lane, acc_s, acc_m);
       uu = seg_end;
     }
   }
