@@ -92,6 +92,10 @@ typedef struct {
     const void *nccl_id;   /* 128-byte ncclUniqueId from cjm_get_nccl_id on rank 0,
                               broadcast by the caller; required when world_size > 1 */
     int device;            /* CUDA device ordinal; -1 (default) = current device */
+    int external_halo;     /* world_size > 1 only: 1 = no NCCL; the caller moves the
+                              halo rows itself between cjm_sweeps calls (rows from
+                              cjm_halo_plan) and combines slab-local residuals.
+                              cjm_solve / cjm_solve_host then return UNSUPPORTED. */
     /* tuning knobs, 0 = automatic */
     int temporal_k;        /* sweeps fused per kernel launch (temporal blocking,
                               SURVEY NEXT-1), 1..4; multi-GPU plans use 1 */
@@ -201,6 +205,28 @@ cjm_status cjm_get_nccl_id(void *out128);
 /* Slab geometry of the 1-D row decomposition (host only): rank g of
  * world_size owns interior rows [floor(g ny / W), floor((g+1) ny / W)). */
 cjm_status cjm_slab(int ny, int world_size, int rank, int *y0, int *ny_local);
+
+/* One halo message of the row-slab decomposition (SURVEY section 8(e), row
+ * a9).  Rows are numbered in the local iterate buffer of the rank:
+ * 0 .. ny_local + 2r - 1, ghost rows included (interior row i at r + i).
+ * The rank sends rows [send_row, send_row + rows) to `peer` and receives the
+ * peer's message into rows [recv_row, recv_row + rows). */
+typedef struct {
+    int peer;
+    int send_row;
+    int recv_row;
+    int rows;
+} cjm_halo_msg;
+
+/* Host-only halo plan of rank `rank` of `world_size` for a global grid of
+ * ny interior rows and stencil reach r: one message per neighbour slab
+ * (0, 1 or 2).  My first r interior rows go to the neighbour above (rank-1),
+ * into its last ghost rows; my last r interior rows go to the neighbour below
+ * (rank+1), into its first ghost rows.  msgs must hold 2 entries.
+ * Errors: INVALID_ARG (sizes, a slab thinner than 2r+1 rows when
+ * world_size > 1, r not 1 or 2). */
+cjm_status cjm_halo_plan(int ny, int r, int world_size, int rank, cjm_halo_msg *msgs,
+                         int *nmsgs);
 
 /* Release every device buffer, graph and communicator of the plan.  NULL is
  * ok.  The field-sized buffers go to the library's device-buffer cache

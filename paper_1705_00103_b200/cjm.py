@@ -30,7 +30,7 @@ STATUS = {0: "CJM_OK", 1: "CJM_ERR_INVALID_ARG", 2: "CJM_ERR_UNSUPPORTED",
 
 # Symbols include/cjm.h declares (tests/test_abi.py checks the header agrees).
 EXPORTS = ("cjm_default_options", "cjm_schedule", "cjm_plan", "cjm_plan_info", "cjm_solve",
-           "cjm_solve_host", "cjm_sweeps", "cjm_residual", "cjm_get_nccl_id", "cjm_slab",
+           "cjm_solve_host", "cjm_sweeps", "cjm_residual", "cjm_get_nccl_id", "cjm_slab", "cjm_halo_plan",
            "cjm_plan_destroy", "cjm_pool_trim", "cjm_status_str", "cjm_last_error", "cjm_version")
 
 
@@ -44,9 +44,14 @@ class CJMError(RuntimeError):
 class Options(C.Structure):
     _fields_ = [("max_cycles", C.c_int), ("order", C.c_int), ("method", C.c_int),
                 ("jacobi_check", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
-                ("nccl_id", C.c_void_p), ("device", C.c_int), ("temporal_k", C.c_int),
+                ("nccl_id", C.c_void_p), ("device", C.c_int), ("external_halo", C.c_int),
+                ("temporal_k", C.c_int),
                 ("tile_w", C.c_int),
                 ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int)]
+
+
+class HaloMsg(C.Structure):
+    _fields_ = [("peer", C.c_int), ("send_row", C.c_int), ("recv_row", C.c_int), ("rows", C.c_int)]
 
 
 class Report(C.Structure):
@@ -91,6 +96,7 @@ def lib():
     L.cjm_residual.argtypes = [vp, vp, ll, vp, ll, vp, dp, dp]
     L.cjm_get_nccl_id.argtypes = [vp]
     L.cjm_slab.argtypes = [i, i, i, C.POINTER(i), C.POINTER(i)]
+    L.cjm_halo_plan.argtypes = [i, i, i, i, C.POINTER(HaloMsg), C.POINTER(i)]
     L.cjm_plan_destroy.argtypes = [vp]
     L.cjm_pool_trim.argtypes = [C.POINTER(ll)]
     L.cjm_status_str.argtypes = [i]
@@ -166,6 +172,16 @@ def cjm_slab(ny: int, world_size: int, rank: int) -> tuple[int, int]:
     y0, n = C.c_int(), C.c_int()
     _check(lib().cjm_slab(ny, world_size, rank, C.byref(y0), C.byref(n)), "cjm_slab")
     return y0.value, n.value
+
+
+def cjm_halo_plan(ny: int, r: int, world_size: int, rank: int) -> list[dict]:
+    """Halo messages of `rank`: dicts with peer, send_row, recv_row, rows
+    (local buffer rows, ghost rows included)."""
+    msgs = (HaloMsg * 2)()
+    n = C.c_int()
+    _check(lib().cjm_halo_plan(ny, r, world_size, rank, msgs, C.byref(n)), "cjm_halo_plan")
+    return [dict(peer=m.peer, send_row=m.send_row, recv_row=m.recv_row, rows=m.rows)
+            for m in msgs[:n.value]]
 
 
 def cjm_get_nccl_id() -> bytes:

@@ -171,23 +171,22 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
   return CJM_OK;
 }
 
-// Halo exchange of the iterate buffer `b` (row a9): my first / last R interior
-// rows to the neighbours' ghost rows.  Rows are contiguous R*ld doubles.
+// Halo exchange of the iterate buffer `b` (row a9), one grouped NCCL
+// send/recv per neighbour as laid out by cjm_halo_plan.  Rows are contiguous
+// (r rows x ld doubles, ghost columns included: they hold the same Dirichlet
+// data on both ranks).
 cjm_status halo_exchange(cjm_plan_s* pl, double* b, cudaStream_t st) {
-  if (pl->world == 1) return CJM_OK;
-  const size_t cnt = (size_t)pl->R * pl->ld;
-  double* first_rows = b + (long long)pl->R * pl->ld;          // interior rows 0..R-1
-  double* last_rows = b + (long long)pl->ny_local * pl->ld;     // interior rows ny-R..ny-1
-  double* ghost_lo = b;                                           // ghost rows -R..-1
-  double* ghost_hi = b + (long long)(pl->ny_local + pl->R) * pl->ld;
+  if (pl->world == 1 || !pl->comm) return CJM_OK;   // external_halo: the caller moves them
+  cjm_halo_msg msgs[2];
+  int nm = 0;
+  STATUS_TRY(cjm_halo_plan(pl->ny, pl->R, pl->world, pl->rank, msgs, &nm));
   NCCL_TRY(ncclGroupStart());
-  if (pl->rank > 0) {
-    NCCL_TRY(ncclSend(first_rows, cnt, ncclDouble, pl->rank - 1, pl->comm, st));
-    NCCL_TRY(ncclRecv(ghost_lo, cnt, ncclDouble, pl->rank - 1, pl->comm, st));
-  }
-  if (pl->rank < pl->world - 1) {
-    NCCL_TRY(ncclSend(last_rows, cnt, ncclDouble, pl->rank + 1, pl->comm, st));
-    NCCL_TRY(ncclRecv(ghost_hi, cnt, ncclDouble, pl->rank + 1, pl->comm, st));
+  for (int k = 0; k < nm; ++k) {
+    const size_t cnt = (size_t)msgs[k].rows * pl->ld;
+    NCCL_TRY(ncclSend(b + (long long)msgs[k].send_row * pl->ld, cnt, ncclDouble, msgs[k].peer,
+                      pl->comm, st));
+    NCCL_TRY(ncclRecv(b + (long long)msgs[k].recv_row * pl->ld, cnt, ncclDouble, msgs[k].peer,
+                      pl->comm, st));
   }
   NCCL_TRY(ncclGroupEnd());
   return CJM_OK;
@@ -252,7 +251,7 @@ cjm_status run_hot(cjm_plan_s* pl, long long count, cudaStream_t st, long long* 
 
 // Sum / max over ranks of the reduction result and D2H of the two scalars.
 cjm_status fetch_result(cjm_plan_s* pl, cudaStream_t st, double* s, double* m) {
-  if (pl->world > 1) {
+  if (pl->world > 1 && pl->comm) {
     NCCL_TRY(ncclGroupStart());
     NCCL_TRY(ncclAllReduce(pl->result, pl->result, 1, ncclDouble, ncclSum, pl->comm, st));
     NCCL_TRY(ncclAllReduce(pl->result + 1, pl->result + 1, 1, ncclDouble, ncclMax, pl->comm, st));
@@ -334,6 +333,10 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
   if (!check_layout(pl, rhs, ld_rhs, u, ld_u) || !rhs) {
     set_error("cjm_solve", "invalid pointer or pitch");
     return CJM_ERR_INVALID_ARG;
+  }
+  if (pl->world > 1 && !pl->comm) {
+    set_error("cjm_solve", "external_halo plans run cjm_sweeps / cjm_residual only");
+    return CJM_ERR_UNSUPPORTED;
   }
   CUDA_TRY(cudaSetDevice(pl->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -461,6 +464,33 @@ cjm_status cjm_slab(int ny, int world_size, int rank, int* y0, int* ny_local) {
   return CJM_OK;
 }
 
+cjm_status cjm_halo_plan(int ny, int r, int world_size, int rank, cjm_halo_msg* msgs,
+                         int* nmsgs) {
+  int y0 = 0, nyl = 0;
+  if (!msgs || !nmsgs || (r != 1 && r != 2) || cjm_slab(ny, world_size, rank, &y0, &nyl) != CJM_OK ||
+      (world_size > 1 && nyl < 2 * r + 1)) {
+    set_error("cjm_halo_plan", "invalid argument");
+    return CJM_ERR_INVALID_ARG;
+  }
+  int n = 0;
+  if (rank > 0) {                    // neighbour above: lower global rows
+    msgs[n].peer = rank - 1;
+    msgs[n].send_row = r;            // my first r interior rows
+    msgs[n].recv_row = 0;            // into my first r ghost rows
+    msgs[n].rows = r;
+    ++n;
+  }
+  if (rank < world_size - 1) {       // neighbour below: higher global rows
+    msgs[n].peer = rank + 1;
+    msgs[n].send_row = nyl;          // my last r interior rows (r + nyl - r)
+    msgs[n].recv_row = nyl + r;      // into my last r ghost rows
+    msgs[n].rows = r;
+    ++n;
+  }
+  *nmsgs = n;
+  return CJM_OK;
+}
+
 cjm_status cjm_get_nccl_id(void* out128) {
   if (!out128) return CJM_ERR_INVALID_ARG;
   ncclUniqueId id;
@@ -506,7 +536,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   const int R = cjm::stencil_reach(stencil);
   if (!R || nx < 4 || ny < 4 || !(h > 0.0) || !std::isfinite(h) || !(tol > 0.0 && tol < 1.0) ||
       opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size ||
-      (opt.world_size > 1 && !opt.nccl_id) ||
+      (opt.world_size > 1 && !opt.nccl_id && !opt.external_halo) ||
       (opt.method != CJM_METHOD_CHEBYSHEV && opt.method != CJM_METHOD_JACOBI) ||
       (opt.tile_w != 0 && opt.tile_w != 256 && opt.tile_w != 512) || opt.stages < 0 ||
       opt.temporal_k < 0 || opt.temporal_k > 4 ||
@@ -625,7 +655,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   PLAN_CUDA(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
   for (auto& e : pl->ev) PLAN_CUDA(cudaEventCreate(&e));
 
-  if (pl->world > 1) {
+  if (pl->world > 1 && !opt.external_halo) {
     ncclUniqueId id;
     std::memcpy(&id, opt.nccl_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&pl->comm, pl->world, id, pl->rank);

@@ -1,0 +1,77 @@
+"""Row-slab decomposition of the CUDA path on ONE GPU (no NCCL).
+
+Each slab is its own plan (world_size=G, external_halo=1: global schedule,
+slab geometry, no communicator); the test moves the halo rows between the
+slab tensors with device copies laid out by cjm_halo_plan (the same host logic
+the NCCL exchange uses) and calls cjm_sweeps one sweep at a time.  Nothing
+waits on anything across slabs (all stream-ordered), so this is a legitimate
+single-GPU check of the slab kernels and the halo geometry: the gathered field
+must be bitwise equal to the single-domain CUDA run and to the oracle.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1705_00103_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1705_00103_b200 import cjm  # noqa: E402
+
+
+@pytest.mark.parametrize("world,stencil,nx,ny", [(2, 9, 300, 257), (4, 17, 130, 97), (3, 5, 64, 200),
+                                                 (8, 9, 513, 64)])
+def test_slabs_bitwise_equal_single_domain(world, stencil, nx, ny):
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=21)
+    nsweeps = 9
+    plans, us, bs, msgs = [], [], [], []
+    for g in range(world):
+        y0, nyl = cjm.cjm_slab(ny, world, g)
+        plans.append(cjm.Plan(stencil, nx, ny, h, 1e-8, world_size=world, rank=g, external_halo=1))
+        assert (plans[-1].y0, plans[-1].ny_local) == (y0, nyl)
+        us.append(torch.from_numpy(u0[y0:y0 + nyl + 2 * r].copy()).cuda())
+        bs.append(torch.from_numpy(b[y0:y0 + nyl].copy()).cuda())
+        msgs.append(cjm.cjm_halo_plan(ny, r, world, g))
+    for k in range(nsweeps):
+        for g in range(world):
+            plans[g].sweeps(bs[g], us[g], k, 1)
+        staged = []
+        for g in range(world):                       # read every send block first
+            for m in msgs[g]:
+                staged.append((m["peer"], g, us[g][m["send_row"]:m["send_row"] + m["rows"]].clone()))
+        for peer, src, blk in staged:
+            m = [x for x in msgs[peer] if x["peer"] == src][0]
+            us[peer][m["recv_row"]:m["recv_row"] + m["rows"]] = blk
+    field = torch.cat([us[g][r:-r] for g in range(world)]).cpu().numpy()
+    with cjm.Plan(stencil, nx, ny, h, 1e-8, temporal_k=1) as whole:
+        ud = torch.from_numpy(u0.copy()).cuda()
+        whole.sweeps(torch.from_numpy(b).cuda(), ud, 0, nsweeps)
+        ref = ud.cpu().numpy()
+    s = oracle.schedule(stencil, nx, ny, 1e-8)
+    uo = oracle.sweeps(stencil, u0, oracle.rhs_to_g(stencil, h, b), s["w"], 0, nsweeps)
+    assert np.array_equal(field, ref[r:-r])
+    assert np.array_equal(field, uo[r:-r])
+    # slab-local residuals combine to the global one
+    l2s, lis = zip(*[plans[g].residual(bs[g], us[g]) for g in range(world)])
+    gl2, gli = oracle.residual(stencil, h, b, np.concatenate([u0[:r], field, u0[-r:]]))
+    assert np.sqrt(sum(x * x for x in l2s)) == pytest.approx(gl2, rel=1e-12)
+    assert max(lis) == gli
+    for p in plans:
+        p.close()
+
+
+def test_external_halo_plan_refuses_solve():
+    u0, b, h = inputs.test_problem(64, 64, 1)
+    with cjm.Plan(9, 64, 64, h, 1e-8, world_size=2, rank=0, external_halo=1) as plan:
+        y0, nyl = plan.y0, plan.ny_local
+        with pytest.raises(cjm.CJMError) as e:
+            plan.solve(torch.from_numpy(b[:nyl].copy()).cuda(),
+                       torch.from_numpy(u0[:nyl + 2].copy()).cuda())
+        assert e.value.name == "CJM_ERR_UNSUPPORTED"
