@@ -25,7 +25,7 @@ sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 from paper_1705_00103_b200 import inputs  # noqa: E402
 
-OUT = os.path.join(ROOT, "tests", "golden", "oracle_digests.json")
+OUT = os.environ.get("CJM_DIGESTS_OUT", os.path.join(ROOT, "tests", "golden", "oracle_digests.json"))
 
 # name -> (stencil, nx, ny, tol, init)   (BASELINE.json configs)
 CONFIGS = {
