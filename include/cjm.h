@@ -99,7 +99,9 @@ typedef struct {
     /* tuning knobs, 0 = automatic */
     int temporal_k;        /* sweeps fused per kernel launch (temporal blocking,
                               SURVEY NEXT-1), 1..4; multi-GPU plans use 1 */
-    int tile_w;            /* tile columns per CTA: 256 or 512 */
+    int variant;           /* sweep kernel: 3 = shared-line levels, 4 = warp-tiled
+                              (default); both bitwise identical */
+    int tile_w;            /* variant 3 only: tile columns per CTA, 256 or 512 */
     int ctas_per_sm;       /* resident CTAs per SM of the persistent sweep grid */
     int stages;            /* depth of the TMA row ring */
     int graph_chunk;       /* sweeps captured per CUDA graph */

@@ -45,7 +45,7 @@ class Options(C.Structure):
     _fields_ = [("max_cycles", C.c_int), ("order", C.c_int), ("method", C.c_int),
                 ("jacobi_check", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
                 ("nccl_id", C.c_void_p), ("device", C.c_int), ("external_halo", C.c_int),
-                ("temporal_k", C.c_int),
+                ("temporal_k", C.c_int), ("variant", C.c_int),
                 ("tile_w", C.c_int),
                 ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int)]
 

@@ -25,6 +25,7 @@
 #include "../../include/cjm.h"
 #include "internal.h"
 #include "sweep.cuh"
+#include "sweep_v4.cuh"
 
 namespace {
 
@@ -86,7 +87,41 @@ KernelFn pick_nt(int NT, int K, int mode) {
   return NT == 256 ? pick_k<ST, 256>(K, mode) : pick_k<ST, 128>(K, mode);
 }
 
-KernelFn pick_kernel(int stencil, int NT, int K, int mode) {
+// warp-tiled variant (sweep_v4.cuh), 4 consumer warps
+template <int ST, int K>
+KernelFn pick_mode_v4(int mode) {
+  switch (mode) {
+    case MODE_HOT: return cjm::cjm_sweep_kernel_v4<ST, 4, K, false, true>;
+    case MODE_CHECK: return cjm::cjm_sweep_kernel_v4<ST, 4, K, true, true>;
+    default: return cjm::cjm_sweep_kernel_v4<ST, 4, 1, true, false>;
+  }
+}
+
+// the 17-point warp-tiled kernel with K >= 2 does not fit the register file
+// (5-row rings of 4 columns x 3 arrays per level): not instantiated, the plan
+// uses the shared-line variant there
+template <int ST>
+KernelFn pick_k_v4(int K, int mode) {
+  if constexpr (ST == 17) {
+    return K == 1 ? pick_mode_v4<ST, 1>(mode) : nullptr;
+  } else {
+    switch (K) {
+      case 1: return pick_mode_v4<ST, 1>(mode);
+      case 2: return pick_mode_v4<ST, 2>(mode);
+      case 3: return pick_mode_v4<ST, 3>(mode);
+      default: return pick_mode_v4<ST, 4>(mode);
+    }
+  }
+}
+
+KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode) {
+  if (variant == 4) {
+    switch (stencil) {
+      case 5: return pick_k_v4<5>(K, mode);
+      case 9: return pick_k_v4<9>(K, mode);
+      default: return pick_k_v4<17>(K, mode);
+    }
+  }
   switch (stencil) {
     case 5: return pick_nt<5>(NT, K, mode);
     case 9: return pick_nt<9>(NT, K, mode);
@@ -127,6 +162,7 @@ struct cjm_plan_s {
   cjm::SweepState* state = nullptr;
   // launch configuration
   int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
+  int variant = 4;   // 3: shared-line levels (sweep.cuh), 4: warp-tiled (sweep_v4.cuh)
   cudaStream_t cap_stream = nullptr;
   std::map<std::pair<long long, int>, cudaGraphExec_t> graphs;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -138,12 +174,32 @@ struct cjm_plan_s {
 
 namespace {
 
+int v4_tout(int R, int K) {      // owned columns per CTA strip, warp-tiled variant
+  const int E = K == 1 ? 0 : ((R * (K - 1) + 1) & ~1);
+  return 4 * (128 - 2 * E);
+}
+
+int tile_out(const cjm_plan_s* pl, int K) {
+  if (pl->variant == 4) return v4_tout(pl->R, K);
+  return 2 * pl->NT - 2 * tile_e(pl->R, K);
+}
+
 size_t smem_bytes(const cjm_plan_s* pl, int K) {
+  if (pl->variant == 4) {
+    const int E = K == 1 ? 0 : ((pl->R * (K - 1) + 1) & ~1);
+    const int WOUT = 128 - 2 * E;
+    const int TG = 3 * WOUT + 128;
+    const int ROW = (TG + 4 + 7) / 8 * 8, GROW = (TG + 7) / 8 * 8;
+    return (size_t)pl->stages * (ROW + GROW) * sizeof(double) +
+           2 * (size_t)pl->stages * sizeof(uint64_t);
+  }
   const int T = 2 * pl->NT, ROW = T + 8;
   return (size_t)pl->stages * (ROW + T) * sizeof(double) +
          (size_t)(K - 1) * (2 * pl->R + 1) * ROW * sizeof(double) +
          2 * (size_t)pl->stages * sizeof(uint64_t);
 }
+
+int block_threads(const cjm_plan_s* pl) { return pl->variant == 4 ? 4 * 32 + 32 : pl->NT + 32; }
 
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur.
 cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
@@ -160,11 +216,11 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
   sp.nx = pl->nx;
   sp.rows = pl->ny_local;
   sp.stages = pl->stages;
-  const int tout = 2 * pl->NT - 2 * tile_e(pl->R, K);
+  const int tout = tile_out(pl, K);
   const long long nstrips = (pl->nx + tout - 1) / tout;
   sp.units = nstrips * pl->ny_local;
-  KernelFn k = pick_kernel(pl->stencil, pl->NT, K, mode);
-  k<<<pl->nctas, pl->NT + 32, smem_bytes(pl, K), st>>>(sp);
+  KernelFn k = pick_kernel(pl->stencil, pl->variant, pl->NT, K, mode);
+  k<<<pl->nctas, block_threads(pl), smem_bytes(pl, K), st>>>(sp);
   CUDA_TRY(cudaGetLastError());
   pl->launches += 1;
   if (mode != MODE_RESID) pl->host_cur ^= 1;
@@ -539,7 +595,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
       (opt.world_size > 1 && !opt.nccl_id && !opt.external_halo) ||
       (opt.method != CJM_METHOD_CHEBYSHEV && opt.method != CJM_METHOD_JACOBI) ||
       (opt.tile_w != 0 && opt.tile_w != 256 && opt.tile_w != 512) || opt.stages < 0 ||
-      opt.temporal_k < 0 || opt.temporal_k > 4 ||
+      opt.temporal_k < 0 || opt.temporal_k > 4 || (opt.variant != 0 && opt.variant != 3 && opt.variant != 4) ||
       opt.stages > 32 || opt.ctas_per_sm < 0 || opt.graph_chunk < 0 || opt.max_cycles < 0 ||
       opt.jacobi_check < 0) {
     set_error("cjm_plan", "invalid argument");
@@ -605,8 +661,18 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   // two sweeps fused per launch, 256-column tiles, 4-row TMA ring, 4 CTAs/SM
   pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 4;
   pl->NT = opt.tile_w == 512 ? 256 : 128;
+  // warp-tiled (4) by default; the 17-point with K >= 2 needs the shared-line
+  // variant (3), whose per-thread state is half as large
+  pl->variant = opt.variant ? opt.variant : 4;
   pl->K = opt.temporal_k > 0 ? opt.temporal_k : 2;
   if (pl->world > 1) pl->K = 1;   // deep halos for K > 1 across ranks: not implemented
+  if (stencil == 17 && pl->K > 1) {
+    if (opt.variant == 4) {
+      set_error("cjm_plan", "variant 4 supports the 17-point stencil with temporal_k = 1 only");
+      return fail(CJM_ERR_INVALID_ARG);
+    }
+    pl->variant = 3;
+  }
   pl->stages = opt.stages > 0 ? opt.stages : 4;
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
   // The grid is sized for the hot kernel (persistent: ctas_per_sm per SM, all
@@ -618,13 +684,13 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
     if (K != 1 && K != pl->K) continue;
     for (int mode = 0; mode < 3; ++mode) {
       if (mode == MODE_RESID && K != 1) continue;
-      KernelFn k = pick_kernel(stencil, pl->NT, K, mode);
+      KernelFn k = pick_kernel(stencil, pl->variant, pl->NT, K, mode);
       const size_t sm = smem_bytes(pl, K);
       PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sm));
       if (K == pl->K && mode == MODE_HOT) {
         PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_min, (const void*)k,
-                                                                pl->NT + 32, sm));
+                                                                block_threads(pl), sm));
       }
     }
   }

@@ -1,0 +1,377 @@
+// sm_100a fp64 CJM sweep kernel, warp-tiled variant (
+// NEXT-1 temporal blocking).
+//
+// Same contract, state machine, producer and reduction as cjm_sweep_kernel
+// (sweep.cuh); the consumer side is organised around independent WARP tiles:
+//  * each lane owns CPL = 4 adjacent columns (LDS.128 / STG.128), a warp spans
+//    128 columns at every level;
+//  * the K on-chip levels hand their rows to the next level IN REGISTERS:
+//    the horizontal neighbours a level needs come from the adjacent lanes
+//    (__shfl_up / __shfl_down), so there is no shared-memory line, no named
+//    barrier and no level skew -- the warps of a CTA only meet at the TMA
+//    ring's mbarriers;
+//  * the price is a lost halo of E = r(K-1) (rounded up to even) columns per
+//    side per WARP (instead of per CTA): a warp owns 128 - 2E output columns
+//    and adjacent warp windows overlap by 2E columns.
+// Everything else (pass-through ghosts, the FAST instantiation, the fixed
+// association of DESIGN R6, device-side n / cur, ticket, fixed-order
+// reduction) is as in sweep.cuh.
+#pragma once
+
+#include "sweep.cuh"
+
+namespace cjm {
+
+template <int R, int K>
+struct WarpGeom {
+  static constexpr int CPL = 4;                               // columns per lane
+  static constexpr int WSPAN = 32 * CPL;                      // warp window
+  static constexpr int E = (K == 1) ? 0 : ((R * (K - 1) + 1) & ~1);
+  static constexpr int WOUT = WSPAN - 2 * E;                  // owned per warp
+};
+
+template <int R, int K, int NW>
+struct TileV4 {
+  using WG = WarpGeom<R, K>;
+  static constexpr int TOUT = NW * WG::WOUT;                  // owned per CTA strip
+  static constexpr int TG = (NW - 1) * WG::WOUT + WG::WSPAN;  // g columns loaded
+  static constexpr int TLOAD = TG + 4;                        // u columns loaded
+  static constexpr int ROW = ((TLOAD + 7) / 8) * 8;           // shared row stride
+  static constexpr int GROW = ((TG + 7) / 8) * 8;
+};
+
+template <int R, int K>
+struct WarpState {
+  static constexpr int P = 2 * R + 1;
+  static constexpr int C = WarpGeom<R, K>::CPL;
+  double u[K][P][C], h1[K][P][C], h2[K][P][C];   // ring slot = step mod P
+  double gr[K][P][C];                            // g of level l-1, for level l R steps later
+  double wl[K];
+  int stage;
+  uint32_t phase;
+  uint32_t full_a, empty_a;
+};
+
+// Push one row of level values (4 centre values + neighbours) into slot `sl`
+// of the level's ring: centre values and pair sums (west + east).
+template <int R, int K>
+__device__ __forceinline__ void push_row(WarpState<R, K>& ws, int l, int sl, const double (&c)[4],
+                                         double l2, double l1, double r1, double r2) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) ws.u[l][sl][j] = c[j];
+  ws.h1[l][sl][0] = __dadd_rn(l1, c[1]);
+  ws.h1[l][sl][1] = __dadd_rn(c[0], c[2]);
+  ws.h1[l][sl][2] = __dadd_rn(c[1], c[3]);
+  ws.h1[l][sl][3] = __dadd_rn(c[2], r1);
+  if (R == 2) {
+    ws.h2[l][sl][0] = __dadd_rn(l2, c[2]);
+    ws.h2[l][sl][1] = __dadd_rn(l1, c[3]);
+    ws.h2[l][sl][2] = __dadd_rn(c[0], r1);
+    ws.h2[l][sl][3] = __dadd_rn(c[1], r2);
+  }
+}
+
+template <int STENCIL, int NW, int K, bool REDUCE, bool STORE, bool FAST>
+__device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws,
+                                             const SweepParams& p, const double* su,
+                                             const double* sg, double* dst, int ja, int jb,
+                                             int c0, int warp, int lane, double& acc_s,
+                                             double& acc_m) {
+  constexpr int R = Point<STENCIL>::R;
+  constexpr int P = 2 * R + 1;
+  using WG = WarpGeom<R, K>;
+  using TG_ = TileV4<R, K, NW>;
+  constexpr int E = WG::E;
+  const long long ld = p.ld;
+  const int rows = p.rows;
+  const int wbase = warp * WG::WOUT;                 // warp window offset in the tile
+  const int cw = c0 + wbase;                         // first column of the warp window
+  const int cl = cw + 4 * lane;                      // first column of this lane
+  bool in[4], own[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = cl + j;
+    in[j] = c >= 0 && c < p.nx;
+    own[j] = in[j] && (4 * lane + j) >= E && (4 * lane + j) < WG::WSPAN - E;
+  }
+  const int nin = jb - ja + 2 * K * R;
+  const int row_base = ja - K * R;
+  double* outp = dst + (long long)(ja + R) * ld + PADL + cl;
+  const int uoff = wbase + 4 * lane;                 // shared index of column cl - 2
+
+  for (int k0 = 0; k0 < nin; k0 += P) {
+#pragma unroll
+    for (int ph = 0; ph < P; ++ph) {
+      const int kk = k0 + ph;
+      if (kk < nin) {
+        // ---- level 0 input: the TMA row of step kk
+        double g0[4] = {0.0, 0.0, 0.0, 0.0};
+        {
+          mbar_wait_a(ws.full_a + 8u * ws.stage, ws.phase);
+          const double* row = su + (size_t)ws.stage * TG_::ROW + uoff;
+          const double2 c01 = *reinterpret_cast<const double2*>(row + 2);
+          const double2 c23 = *reinterpret_cast<const double2*>(row + 4);
+          double l2 = 0.0, l1, r1, r2 = 0.0;
+          if (R == 2) {
+            const double2 lft = *reinterpret_cast<const double2*>(row);
+            const double2 rgt = *reinterpret_cast<const double2*>(row + 6);
+            l2 = lft.x; l1 = lft.y; r1 = rgt.x; r2 = rgt.y;
+          } else {
+            l1 = row[1];
+            r1 = row[6];
+          }
+          if (kk >= 2 * R) {
+            const double* grow = sg + (size_t)ws.stage * TG_::GROW + uoff;
+            const double2 ga = *reinterpret_cast<const double2*>(grow);
+            const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
+            g0[0] = ga.x; g0[1] = ga.y; g0[2] = gb.x; g0[3] = gb.y;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * ws.stage);
+          if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
+          const double cc[4] = {c01.x, c01.y, c23.x, c23.y};
+          push_row<R, K>(ws, 0, ph, cc, l2, l1, r1, r2);
+        }
+        // ---- levels, in order; level l hands its row to level l+1 in registers
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+          double g[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) g[j] = (l == 0) ? g0[j] : ws.gr[l][(ph + P - R) % P][j];
+          if (l + 1 < K) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ws.gr[l + 1][ph][j] = g[j];
+          }
+          if (kk >= 2 * (l + 1) * R) {
+            const int G = row_base + kk - (l + 1) * R;           // global row of the output
+            const bool rowin = (unsigned)G < (unsigned)rows;
+            double o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              double uw[P], x1[P], x2[P];
+#pragma unroll
+              for (int q = 0; q < P; ++q) {                      // logical row q -> slot
+                const int sl = (ph + 1 + q) % P;
+                uw[q] = ws.u[l][sl][j];
+                x1[q] = ws.h1[l][sl][j];
+                x2[q] = ws.h2[l][sl][j];
+              }
+              const double J = Point<STENCIL>::jacobi_target(uw, x1, x2, g[j]);
+              const double d = __dsub_rn(J, uw[R]);
+              o[j] = (FAST || (rowin && in[j])) ? __fma_rn(ws.wl[l], d, uw[R]) : uw[R];
+              if (REDUCE && l == 0 && (unsigned)(G - ja) < (unsigned)(jb - ja) && own[j]) {
+                acc_s = __fma_rn(d, d, acc_s);
+                acc_m = nan_max(acc_m, fabs(d));
+              }
+            }
+            if (l + 1 < K) {
+              // neighbours of this lane's columns at level l: adjacent lanes
+              const double l1 = __shfl_up_sync(0xffffffffu, o[3], 1);
+              const double r1 = __shfl_down_sync(0xffffffffu, o[0], 1);
+              double l2 = 0.0, r2 = 0.0;
+              if (R == 2) {
+                l2 = __shfl_up_sync(0xffffffffu, o[2], 1);
+                r2 = __shfl_down_sync(0xffffffffu, o[1], 1);
+              }
+              push_row<R, K>(ws, l + 1, ph, o, l2, l1, r1, r2);
+            } else {
+              if (STORE) {
+                // FAST: every column is interior, ownership depends on the lane only
+                // (E even: both columns of a pair are owned or neither)
+                const bool own01 = FAST ? (4 * lane >= E && 4 * lane + 2 <= WG::WSPAN - E)
+                                        : (own[0] && own[1]);
+                const bool own23 = FAST ? (4 * lane + 2 >= E && 4 * lane + 4 <= WG::WSPAN - E)
+                                        : (own[2] && own[3]);
+                if (own01) *reinterpret_cast<double2*>(outp) = make_double2(o[0], o[1]);
+                else if (!FAST) {
+                  if (own[0]) outp[0] = o[0];
+                  if (own[1]) outp[1] = o[1];
+                }
+                if (own23) *reinterpret_cast<double2*>(outp + 2) = make_double2(o[2], o[3]);
+                else if (!FAST) {
+                  if (own[2]) outp[2] = o[2];
+                  if (own[3]) outp[3] = o[3];
+                }
+              }
+              outp += ld;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int STENCIL, int NW, int K, bool REDUCE, bool STORE>
+__global__ void __launch_bounds__(32 * NW + 32)
+cjm_sweep_kernel_v4(const SweepParams p) {
+  constexpr int R = Point<STENCIL>::R;
+  using WG = WarpGeom<R, K>;
+  using TG_ = TileV4<R, K, NW>;
+  constexpr int E = WG::E;
+  constexpr int NT = 32 * NW;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* su = reinterpret_cast<double*>(smem_raw);
+  double* sg = su + (size_t)p.stages * TG_::ROW;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sg + (size_t)p.stages * TG_::GROW);
+  uint64_t* empty = full + p.stages;
+  __shared__ double red_s[NW], red_m[NW];
+  __shared__ int is_last;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+
+  if (tid == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const unsigned long long n = __ldcg(&p.state->n);
+  const unsigned int cur = __ldcg(&p.state->cur);
+  const double* src = (cur & 1u) ? p.buf[1] : p.buf[0];
+  double* dst = (cur & 1u) ? p.buf[0] : p.buf[1];
+  const long long ld = p.ld;
+  const int rows = p.rows;
+  const long long u_begin = (long long)blockIdx.x * p.units / gridDim.x;
+  const long long u_end = (long long)(blockIdx.x + 1) * p.units / gridDim.x;
+
+  double acc_s = 0.0, acc_m = 0.0;
+
+  if (tid >= NT) {
+    // ------------------------------------------------ producer warp (lane 0)
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      long long used = 0;
+      const uint32_t full_a = smem_addr(full), empty_a = smem_addr(empty);
+      for (long long uu = u_begin; uu < u_end;) {
+        const int strip = (int)(uu / rows);
+        const int ja = (int)(uu - (long long)strip * rows);
+        const long long seg_end = min(u_end, (long long)(strip + 1) * rows);
+        const int jb = ja + (int)(seg_end - uu);
+        const int c0 = strip * TG_::TOUT - E;
+        const int ucols = min(TG_::TLOAD, p.nx + R + 2 - c0);
+        const uint32_t ubytes = (uint32_t)(((ucols + 1) & ~1) * 8);
+        const int gc0 = max(c0, 0);
+        const int gcols = min(c0 + TG_::TG, p.nx) - gc0;
+        const uint32_t gbytes = gcols > 0 ? (uint32_t)(((gcols + 1) & ~1) * 8) : 0u;
+        const int nin = jb - ja + 2 * K * R;
+        for (int k = 0; k < nin; ++k) {
+          if (used >= p.stages) mbar_wait_a(empty_a + 8u * stage, phase ^ 1u);
+          const int gin = ja - K * R + k;
+          const bool hasu = gin >= -R && gin < rows + R;
+          const int g1 = gin - R;
+          const bool hasg = k >= 2 * R && g1 >= 0 && g1 < rows && gbytes;
+          mbar_arrive_expect_tx(&full[stage], (hasu ? ubytes : 0u) + (hasg ? gbytes : 0u));
+          if (hasu)
+            tma_row_load(su + (size_t)stage * TG_::ROW,
+                         src + (long long)(gin + R) * ld + (PADL - 2) + c0, ubytes, &full[stage], pol);
+          if (hasg)
+            tma_row_load(sg + (size_t)stage * TG_::GROW + (gc0 - c0),
+                         p.g + (long long)g1 * ld + PADL + gc0, gbytes, &full[stage], pol);
+          ++used;
+          if (++stage == p.stages) { stage = 0; phase ^= 1u; }
+        }
+        uu = seg_end;
+      }
+    }
+  } else {
+    // ---------------------------------------------- consumer warps
+    WarpState<R, K> ws;
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+      ws.wl[l] = __ldg(p.w + (long long)((n + l) % (unsigned long long)p.P));
+#pragma unroll
+      for (int q = 0; q < 2 * R + 1; ++q)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ws.u[l][q][j] = ws.h1[l][q][j] = ws.h2[l][q][j] = ws.gr[l][q][j] = 0.0;
+    }
+    ws.stage = 0;
+    ws.phase = 0;
+    ws.full_a = smem_addr(full);
+    ws.empty_a = smem_addr(empty);
+    for (long long uu = u_begin; uu < u_end;) {
+      const int strip = (int)(uu / rows);
+      const int ja = (int)(uu - (long long)strip * rows);
+      const long long seg_end = min(u_end, (long long)(strip + 1) * rows);
+      const int jb = ja + (int)(seg_end - uu);
+      const int c0 = strip * TG_::TOUT - E;
+      const bool fast = ja - K * R >= 0 && jb + K * R <= rows && c0 >= 0 && c0 + TG_::TG <= p.nx;
+      if (fast)
+        warp_segment<STENCIL, NW, K, REDUCE, STORE, true>(ws, p, su, sg, dst, ja, jb, c0, warp, lane,
+                                                          acc_s, acc_m);
+      else
+        warp_segment<STENCIL, NW, K, REDUCE, STORE, false>(ws, p, su, sg, dst, ja, jb, c0, warp, lane,
+                                                           acc_s, acc_m);
+      uu = seg_end;
+    }
+  }
+
+  if (REDUCE) {
+    if (tid < NT) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc_s = __dadd_rn(acc_s, __shfl_xor_sync(0xffffffffu, acc_s, o));
+        acc_m = nan_max(acc_m, __shfl_xor_sync(0xffffffffu, acc_m, o));
+      }
+      if (lane == 0) { red_s[warp] = acc_s; red_m[warp] = acc_m; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0, m = 0.0;
+      for (int q = 0; q < NW; ++q) { s = __dadd_rn(s, red_s[q]); m = nan_max(m, red_m[q]); }
+      p.partials[2 * blockIdx.x] = s;
+      p.partials[2 * blockIdx.x + 1] = m;
+    }
+  }
+
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int t = atomicAdd(&p.state->ticket, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    if (REDUCE) {
+      double s = 0.0, m = 0.0;
+      if (tid < NT) {
+        for (int b = tid; b < (int)gridDim.x; b += NT) {
+          s = __dadd_rn(s, __ldcg(p.partials + 2 * b));
+          m = nan_max(m, __ldcg(p.partials + 2 * b + 1));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+          m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        }
+        if (lane == 0) { red_s[warp] = s; red_m[warp] = m; }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s = 0.0; m = 0.0;
+        for (int q = 0; q < NW; ++q) { s = __dadd_rn(s, red_s[q]); m = nan_max(m, red_m[q]); }
+        p.result[0] = s;
+        p.result[1] = m;
+      }
+    }
+    if (tid == 0) {
+      if (STORE) {
+        p.state->n = n + (unsigned long long)K;
+        p.state->cur = cur ^ 1u;
+      }
+      p.state->ticket = 0u;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace cjm

@@ -8,8 +8,9 @@ for line in sys.stdin:
     m = re.search(r"Compiling entry function '(\S+)'", line)
     if m:
         name = m.group(1)
-        k = re.search(r"cjm_sweep_kernelILi(\d+)ELi(\d+)ELi(\d+)ELb([01])ELb([01])", name)
-        cur = f"sweep<{k.group(1)},{k.group(2)},K{k.group(3)},red{k.group(4)},st{k.group(5)}>" if k else name[:40]
+        k = re.search(r"cjm_sweep_kernel(_v4)?ILi(\d+)ELi(\d+)ELi(\d+)ELb([01])ELb([01])", name)
+        cur = (f"sweep{k.group(1) or ''}<{k.group(2)},{k.group(3)},K{k.group(4)},red{k.group(5)},st{k.group(6)}>"
+               if k else name[:40])
         rows[cur] = {}
         continue
     if cur is None:

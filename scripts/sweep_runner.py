@@ -43,16 +43,23 @@ if __name__ == "__main__":
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--temporal-k", type=int, default=0)
     ap.add_argument("--ks", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
+    ap.add_argument("--variants", type=lambda v: [int(x) for x in v.split(",")], default=[3, 4])
+    ap.add_argument("--variant", type=int, default=0)
     a = ap.parse_args()
     if a.tune:
         for cfgname in a.config.split(","):
-            for K, tw, stg, cps in itertools.product(a.ks, (256, 512), (4, 8, 12), (1, 2, 3, 4)):
+            grid = []
+            for var in a.variants:
+                tws = (256, 512) if var == 3 else (256,)
+                grid += [(var, K, tw, stg, cps) for K in a.ks for tw in tws for stg in (4, 8, 12)
+                         for cps in (1, 2, 3, 4)]
+            for var, K, tw, stg, cps in grid:
                 try:
-                    print(json.dumps(run(cfgname, 2400, 240, tile_w=tw, stages=stg, ctas_per_sm=cps,
-                                         temporal_k=K)), flush=True)
+                    print(json.dumps(run(cfgname, 2400, 240, variant=var, tile_w=tw, stages=stg,
+                                         ctas_per_sm=cps, temporal_k=K)), flush=True)
                 except Exception as e:  # noqa: BLE001
-                    print(json.dumps(dict(config=cfgname, tile_w=tw, stages=stg, ctas_per_sm=cps,
-                                          temporal_k=K, error=str(e))), flush=True)
+                    print(json.dumps(dict(config=cfgname, variant=var, tile_w=tw, stages=stg,
+                                          ctas_per_sm=cps, temporal_k=K, error=str(e))), flush=True)
     else:
         print(json.dumps(run(a.config, a.count, a.warm, tile_w=a.tile_w, stages=a.stages,
-                             ctas_per_sm=a.ctas_per_sm, temporal_k=a.temporal_k)))
+                             ctas_per_sm=a.ctas_per_sm, temporal_k=a.temporal_k, variant=a.variant)))

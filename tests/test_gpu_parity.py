@@ -56,11 +56,11 @@ SHAPES = [(8, 8), (64, 64), (100, 37), (257, 300), (513, 70), (1000, 11), (4, 4)
 
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("nx,ny", SHAPES)
-@pytest.mark.parametrize("tile_w", (256, 512))
-def test_one_sweep_bitwise(stencil, nx, ny, tile_w):
+@pytest.mark.parametrize("tile_w,variant", [(256, 3), (512, 3), (0, 4)])
+def test_one_sweep_bitwise(stencil, nx, ny, tile_w, variant):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=inputs.SEED_BASE + nx + 7 * ny)
-    with cjm.Plan(stencil, nx, ny, h, 1e-8, tile_w=tile_w) as plan:
+    with cjm.Plan(stencil, nx, ny, h, 1e-8, tile_w=tile_w, variant=variant) as plan:
         w = plan.info()["weights"]
         g = oracle.rhs_to_g(stencil, h, b)
         for first in (0, 1, plan.P - 1):
@@ -75,13 +75,17 @@ def test_one_sweep_bitwise(stencil, nx, ny, tile_w):
 @pytest.mark.parametrize("nx,ny,count", [(300, 257, 37), (1030, 515, 20), (64, 64, 324),
                                          (9, 700, 13), (520, 6, 11)])
 @pytest.mark.parametrize("temporal_k", (1, 2, 3, 4))
-def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k):
+@pytest.mark.parametrize("variant", (3, 4))
+def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
     """A run of sweeps through the CUDA-graph hot loop (spans several graph
     chunks when count > graph_chunk), K sweeps fused per launch (temporal
-    blocking), vs the oracle sweep by sweep."""
+    blocking), both kernel variants, vs the oracle sweep by sweep."""
+    if stencil == 17 and variant == 4 and temporal_k > 1:
+        pytest.skip("17-point warp-tiled kernel is K=1 only (plan picks variant 3)")
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=3)
-    with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=4, temporal_k=temporal_k) as plan:
+    with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=4, temporal_k=temporal_k,
+                  variant=variant) as plan:
         w = plan.info()["weights"]
         ud = dev(u0)
         plan.sweeps(dev(b), ud, 5, count)
@@ -95,8 +99,10 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k):
 @pytest.mark.parametrize("cfg", [dict(tile_w=256, stages=4, ctas_per_sm=1),
                                  dict(tile_w=512, stages=16, ctas_per_sm=3),
                                  dict(tile_w=256, stages=32, ctas_per_sm=2, graph_chunk=7),
-                                 dict(tile_w=512, temporal_k=3, stages=6),
-                                 dict(tile_w=256, temporal_k=4, ctas_per_sm=4)])
+                                 dict(tile_w=512, temporal_k=3, stages=6, variant=3),
+                                 dict(tile_w=256, temporal_k=4, ctas_per_sm=4, variant=3),
+                                 dict(variant=4, temporal_k=3, stages=8, ctas_per_sm=1),
+                                 dict(variant=4, temporal_k=1, stages=2)])
 def test_launch_configuration_does_not_change_result(cfg):
     nx, ny = 777, 301
     u0, b, h = inputs.test_problem(nx, ny, 1, init="random", seed=5)
@@ -125,12 +131,14 @@ def test_residual_matches_oracle(stencil):  # noqa: D103
 # ------------------------------------------------------------ full solves
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("n,init", [(64, "zero"), (64, "random"), (200, "zero"), (129, "random")])
-@pytest.mark.parametrize("temporal_k", (1, 2, 4))
-def test_solve_matches_oracle(stencil, n, init, temporal_k):
+@pytest.mark.parametrize("temporal_k,variant", [(1, 4), (2, 4), (2, 3), (4, 3), (3, 0)])
+def test_solve_matches_oracle(stencil, n, init, temporal_k, variant):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(n, n, r, init=init)
     uo, ro = oracle.solve(stencil, h, 1e-8, b, u0)
-    with cjm.Plan(stencil, n, n, h, 1e-8, temporal_k=temporal_k) as plan:
+    if stencil == 17 and variant == 4 and temporal_k > 1:
+        variant = 0
+    with cjm.Plan(stencil, n, n, h, 1e-8, temporal_k=temporal_k, variant=variant) as plan:
         ud = dev(u0)
         rep = plan.solve(dev(b), ud)
     assert rep["status"] == "CJM_OK" and ro["status"] == "OK"
@@ -224,7 +232,7 @@ def _digest_cases():
 
 @pytest.mark.parametrize("name", _digest_cases())
 @pytest.mark.parametrize("temporal_k", (1, 2))
-def test_solve_matches_stored_oracle_digest(name, temporal_k):
+def test_solve_matches_stored_oracle_digest(name, temporal_k):  # noqa: D103
     """Full solves at BASELINE sizes vs the oracle's stored result
     (tests/make_oracle_digests.py): same iterations, sampled nodes within
     1e-10 max|u| and bitwise, and the SHA-256 of the whole interior."""
