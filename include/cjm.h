@@ -124,6 +124,7 @@ typedef struct {
     long long hot_launches;    /* sweep-kernel launches inside sweep_s */
     int temporal_k;            /* sweeps per hot launch */
     double h2d_bytes, d2h_bytes;  /* host<->device bytes moved by the call */
+    double real_error;     /* cjm_solve_ref: max |u - u_ref| of the returned iterate */
 } cjm_report;
 
 typedef struct cjm_plan_s *cjm_plan_t;
@@ -177,6 +178,19 @@ cjm_status cjm_plan_info(cjm_plan_t p, cjm_report *info, int *reach,
 cjm_status cjm_solve(cjm_plan_t p, const double *rhs, long long ld_rhs,
                      double *u, long long ld_u, void *cuda_stream,
                      cjm_report *rep);
+
+/* The solve with the paper's "real error" stop ("we can use the
+ * real error instead of a tolerance as the stopping criterion"): stop at the
+ * first cycle boundary whose iterate has max |u - u_ref| <= real_tol over the
+ * interior.  u_ref (device, ny_local x nx, pitch ld_ref, read only) holds the
+ * analytic solution at the nodes.  The plan's tol still sets the cycle
+ * length; the residual is still reduced every cycle (report, divergence and
+ * stagnation: a real_tol below the discretisation error ends STAGNATED or
+ * NOT_CONVERGED).  rep->real_error receives the error of the returned iterate.
+ * Errors: INVALID_ARG for a NULL u_ref, ld_ref < nx or real_tol <= 0. */
+cjm_status cjm_solve_ref(cjm_plan_t p, const double *rhs, long long ld_rhs,
+                         double *u, long long ld_u, const double *u_ref, long long ld_ref,
+                         double real_tol, void *cuda_stream, cjm_report *rep);
 
 /* The same solve with HOST buffers: one host->device copy of u and rhs at
  * the start and one device->host copy of the solution at the end (the

@@ -30,6 +30,7 @@ STATUS = {0: "CJM_OK", 1: "CJM_ERR_INVALID_ARG", 2: "CJM_ERR_UNSUPPORTED",
 
 # Symbols include/cjm.h declares (tests/test_abi.py checks the header agrees).
 EXPORTS = ("cjm_default_options", "cjm_schedule", "cjm_plan", "cjm_plan_info", "cjm_solve",
+           "cjm_solve_ref",
            "cjm_solve_host", "cjm_sweeps", "cjm_residual", "cjm_get_nccl_id", "cjm_slab", "cjm_halo_plan",
            "cjm_plan_destroy", "cjm_pool_trim", "cjm_status_str", "cjm_last_error", "cjm_version")
 
@@ -63,7 +64,7 @@ class Report(C.Structure):
                 ("plan_s", C.c_double), ("solve_s", C.c_double), ("sweep_s", C.c_double),
                 ("sweeps_timed", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("hot_launches", C.c_longlong), ("temporal_k", C.c_int),
-                ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double)]
+                ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("real_error", C.c_double)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -92,6 +93,7 @@ def lib():
                                 C.POINTER(dp)]
     L.cjm_solve.argtypes = [vp, vp, ll, vp, ll, vp, C.POINTER(Report)]
     L.cjm_solve_host.argtypes = [vp, vp, ll, vp, ll, vp, C.POINTER(Report)]
+    L.cjm_solve_ref.argtypes = [vp, vp, ll, vp, ll, vp, ll, C.c_double, vp, C.POINTER(Report)]
     L.cjm_sweeps.argtypes = [vp, vp, ll, vp, ll, ll, ll, vp, C.POINTER(Report)]
     L.cjm_residual.argtypes = [vp, vp, ll, vp, ll, vp, dp, dp]
     L.cjm_get_nccl_id.argtypes = [vp]
@@ -233,6 +235,19 @@ class Plan:
         _check(lib().cjm_solve(self._h, rp, rl, up, ul, _stream(stream), C.byref(rep)), "cjm_solve", ok)
         return rep.as_dict()
 
+    def solve_ref(self, rhs, u, u_ref, real_tol: float, stream=None, ok=(0,)) -> dict:
+        """cjm_solve_ref: stop on max|u - u_ref| <= real_tol."""
+        self._check_shapes(rhs, u)
+        if tuple(u_ref.shape) != (self.ny_local, self.nx):
+            raise ValueError("u_ref: interior shape (ny_local, nx) expected")
+        rp, rl = _dev_ptr(rhs, "rhs")
+        up, ul = _dev_ptr(u, "u")
+        ep, el = _dev_ptr(u_ref, "u_ref")
+        rep = Report()
+        _check(lib().cjm_solve_ref(self._h, rp, rl, up, ul, ep, el, real_tol, _stream(stream),
+                                   C.byref(rep)), "cjm_solve_ref", ok)
+        return rep.as_dict()
+
     def solve_host(self, rhs, u, stream=None, ok=(0,)) -> dict:
         """cjm_solve_host on host arrays; u is updated in place."""
         self._check_shapes(rhs, u)
@@ -289,6 +304,10 @@ def cjm_plan_info(plan: Plan) -> dict:
 
 def cjm_solve(plan: Plan, rhs, u, stream=None) -> dict:
     return plan.solve(rhs, u, stream)
+
+
+def cjm_solve_ref(plan: Plan, rhs, u, u_ref, real_tol, stream=None) -> dict:
+    return plan.solve_ref(rhs, u, u_ref, real_tol, stream)
 
 
 def cjm_solve_host(plan: Plan, rhs, u, stream=None) -> dict:

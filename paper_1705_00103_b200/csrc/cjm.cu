@@ -160,6 +160,7 @@ struct cjm_plan_s {
   double* result = nullptr;
   double* result_host = nullptr;  // pinned, 2 doubles
   cjm::SweepState* state = nullptr;
+  unsigned long long* err_bits = nullptr;   // real-error reduction (cjm_solve_ref)
   // launch configuration
   int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
   int variant = 4;   // 3: shared-line levels (sweep.cuh), 4: warp-tiled (sweep_v4.cuh)
@@ -320,6 +321,26 @@ cjm_status fetch_result(cjm_plan_s* pl, cudaStream_t st, double* s, double* m) {
   return CJM_OK;
 }
 
+// max |u_which - u_ref| over the (global) interior.
+cjm_status real_error(cjm_plan_s* pl, int which, const double* ref, long long ld_ref,
+                      cudaStream_t st, double* err) {
+  CUDA_TRY(cudaMemsetAsync(pl->err_bits, 0, sizeof(unsigned long long), st));
+  const long long total = (long long)pl->nx * pl->ny_local;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+  cjm::cjm_error_kernel<<<blocks, 256, 0, st>>>(pl->buf[which], pl->ld, pl->R, ref, ld_ref, pl->nx,
+                                                pl->ny_local, pl->err_bits);
+  CUDA_TRY(cudaGetLastError());
+  pl->launches += 1;
+  if (pl->world > 1 && pl->comm) {
+    double* d = reinterpret_cast<double*>(pl->err_bits);
+    NCCL_TRY(ncclAllReduce(d, d, 1, ncclDouble, ncclMax, pl->comm, st));
+  }
+  CUDA_TRY(cudaMemcpyAsync(pl->result_host, pl->err_bits, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *err = pl->result_host[0];
+  return CJM_OK;
+}
+
 cjm_status set_state(cjm_plan_s* pl, unsigned long long n, cudaStream_t st) {
   set_state_kernel<<<1, 1, 0, st>>>(pl->state, n);
   CUDA_TRY(cudaGetLastError());
@@ -385,8 +406,10 @@ void fill_static(const cjm_plan_s* pl, cjm_report* r) {
 // The whole solve (rows a5-a10); `kin` / `kout` select device or host user buffers.
 cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, double* u,
                       long long ld_u, cudaMemcpyKind kin, cudaMemcpyKind kout, void* stream,
-                      cjm_report* rep_out) {
-  if (!check_layout(pl, rhs, ld_rhs, u, ld_u) || !rhs) {
+                      cjm_report* rep_out, const double* ref = nullptr, long long ld_ref = 0,
+                      double real_tol = 0.0) {
+  if (!check_layout(pl, rhs, ld_rhs, u, ld_u) || !rhs ||
+      (ref && (ld_ref < pl->nx || !(real_tol > 0.0)))) {
     set_error("cjm_solve", "invalid pointer or pitch");
     return CJM_ERR_INVALID_ARG;
   }
@@ -420,10 +443,15 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
   rep.r0_linf = m / sc;
   rep.r_l2 = rep.r0_l2;
   rep.r_linf = rep.r0_linf;
+  double err = 0.0;
+  if (ref) {
+    STATUS_TRY(real_error(pl, check_in, ref, ld_ref, st, &err));
+    rep.real_error = err;
+  }
 
   int status = CJM_ERR_NOT_CONVERGED;
   int out_buf = check_in;                 // buffer of the exported iterate
-  if (rep.r0_l2 == 0.0) {
+  if (ref ? err <= real_tol : rep.r0_l2 == 0.0) {
     status = CJM_OK;
   } else if (!std::isfinite(rep.r0_l2)) {
     status = CJM_ERR_DIVERGED;
@@ -445,7 +473,14 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
       rep.r_linf = m / sc;
       out_buf = check_in;
       if (!std::isfinite(rho)) { status = CJM_ERR_DIVERGED; break; }
-      if (rho <= pl->tol * rep.r0_l2) { status = CJM_OK; break; }
+      if (ref) {   // the paper's real-error stop, checked per cycle
+        STATUS_TRY(real_error(pl, check_in, ref, ld_ref, st, &err));
+        rep.real_error = err;
+        if (err <= real_tol) { status = CJM_OK; break; }
+      } else if (rho <= pl->tol * rep.r0_l2) {
+        status = CJM_OK;
+        break;
+      }
       if (pl->method == CJM_METHOD_CHEBYSHEV && rho > 0.5 * rho_prev) {
         status = CJM_ERR_STAGNATED;
         break;
@@ -571,6 +606,7 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   cudaFree(p->partials);
   cudaFree(p->result);
   cudaFree(p->state);
+  cudaFree(p->err_bits);
   if (p->result_host) cudaFreeHost(p->result_host);
   if (p->comm) ncclCommDestroy(p->comm);
   delete p;
@@ -716,6 +752,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   PLAN_CUDA(cudaMalloc(&pl->partials, (size_t)pl->nctas * 2 * sizeof(double)));
   PLAN_CUDA(cudaMalloc(&pl->result, 2 * sizeof(double)));
   PLAN_CUDA(cudaMalloc(&pl->state, sizeof(cjm::SweepState)));
+  PLAN_CUDA(cudaMalloc(&pl->err_bits, sizeof(unsigned long long)));
   PLAN_CUDA(cudaMemset(pl->state, 0, sizeof(cjm::SweepState)));
   PLAN_CUDA(cudaMallocHost(&pl->result_host, 2 * sizeof(double)));
   PLAN_CUDA(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
@@ -752,6 +789,17 @@ cjm_status cjm_solve(cjm_plan_t p, const double* rhs, long long ld_rhs, double* 
                      void* cuda_stream, cjm_report* rep) {
   return solve_impl(p, rhs, ld_rhs, u, ld_u, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice,
                     cuda_stream, rep);
+}
+
+cjm_status cjm_solve_ref(cjm_plan_t p, const double* rhs, long long ld_rhs, double* u, long long ld_u,
+                         const double* u_ref, long long ld_ref, double real_tol, void* cuda_stream,
+                         cjm_report* rep) {
+  if (!u_ref) {
+    set_error("cjm_solve_ref", "u_ref is NULL");
+    return CJM_ERR_INVALID_ARG;
+  }
+  return solve_impl(p, rhs, ld_rhs, u, ld_u, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice,
+                    cuda_stream, rep, u_ref, ld_ref, real_tol);
 }
 
 cjm_status cjm_solve_host(cjm_plan_t p, const double* rhs_host, long long ld_rhs, double* u_host,

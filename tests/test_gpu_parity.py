@@ -259,3 +259,40 @@ def test_solve_matches_stored_oracle_digest(name, temporal_k):  # noqa: D103
     assert np.array_equal(flat[idx], want)
     assert np.max(np.abs(u)) == rec["max_abs_u"]
     assert hashlib.sha256(np.ascontiguousarray(u, dtype="<f8").tobytes()).hexdigest() == rec["sha256"]
+
+
+# ------------------------------------------------------------ real-error stop (NEXT-3)
+@pytest.mark.parametrize("stencil,n,real_tol", [(17, 127, 1e-8), (5, 63, 1e-6), (9, 100, 1e-4)])
+def test_real_error_stop_matches_oracle_cycles(stencil, n, real_tol):
+    """cjm_solve_ref stops at the first cycle boundary with max|u - u_exact|
+    <= real_tol; the oracle, cycle by cycle, must agree on the
+    cycle and the field (bitwise)."""
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(n, n, r)
+    ex = inputs.exact_field(n, n, r, h)
+    s = oracle.schedule(stencil, n, n, 1e-8)
+    g = oracle.rhs_to_g(stencil, h, b)
+    u, cycles = u0, 0
+    while True:
+        u = oracle.sweeps(stencil, u, g, s["w"], 0, s["P"])
+        cycles += 1
+        if np.max(np.abs(u[r:-r, r:-r] - ex)) <= real_tol or cycles > 8:
+            break
+    with cjm.Plan(stencil, n, n, h, 1e-8) as plan:
+        ud = dev(u0)
+        rep = plan.solve_ref(dev(b), ud, dev(ex), real_tol)
+    assert rep["status"] == "CJM_OK" and rep["cycles"] == cycles
+    assert rep["iterations"] == cycles * s["P"]
+    assert rep["real_error"] == np.max(np.abs(host(ud)[r:-r, r:-r] - ex))
+    assert rep["real_error"] <= real_tol
+    assert_field_parity(host(ud), u, r)
+
+
+def test_real_error_below_discretisation_error_does_not_converge():
+    n = 63
+    u0, b, h = inputs.test_problem(n, n, 1)
+    ex = inputs.exact_field(n, n, 1, h)
+    with cjm.Plan(9, n, n, h, 1e-8, max_cycles=4) as plan:
+        rep = plan.solve_ref(dev(b), dev(u0), dev(ex), 1e-9, ok=(3, 5))
+    assert rep["status"] in ("CJM_ERR_STAGNATED", "CJM_ERR_NOT_CONVERGED")
+    assert rep["real_error"] > 1e-9
