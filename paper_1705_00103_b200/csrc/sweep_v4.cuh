@@ -71,6 +71,120 @@ __device__ __forceinline__ void push_row(WarpState<R, K>& ws, int l, int sl, con
   }
 }
 
+// Per-segment constants of one lane.
+struct LaneSeg {
+  bool in[4], own[4];
+  int ja, jb, row_base, uoff;
+  double* outp;
+};
+
+// One step (input row kk, ring slot ph = kk mod P) of a lane: read the TMA row,
+// run every level (unconditionally: a level computes garbage until its window
+// is full, which is never stored), store the last level when it is active.
+template <int STENCIL, int NW, int K, bool REDUCE, bool STORE, bool FAST>
+__device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, LaneSeg& ls,
+                                          const SweepParams& p, const double* su, const double* sg,
+                                          int kk, int ph, int lane, double& acc_s, double& acc_m) {
+  constexpr int R = Point<STENCIL>::R;
+  constexpr int P = 2 * R + 1;
+  using WG = WarpGeom<R, K>;
+  using TG_ = TileV4<R, K, NW>;
+  constexpr int E = WG::E;
+  // ---- level 0 input: the TMA row of step kk
+  double g0[4];
+  {
+    mbar_wait_a(ws.full_a + 8u * ws.stage, ws.phase);
+    const double* row = su + (size_t)ws.stage * TG_::ROW + ls.uoff;
+    const double2 c01 = *reinterpret_cast<const double2*>(row + 2);
+    const double2 c23 = *reinterpret_cast<const double2*>(row + 4);
+    double l2 = 0.0, l1, r1, r2 = 0.0;
+    if (R == 2) {
+      const double2 lft = *reinterpret_cast<const double2*>(row);
+      const double2 rgt = *reinterpret_cast<const double2*>(row + 6);
+      l2 = lft.x; l1 = lft.y; r1 = rgt.x; r2 = rgt.y;
+    } else {
+      l1 = row[1];
+      r1 = row[6];
+    }
+    // g of the level-0 output row (stale before kk = 2R: never used then)
+    const double* grow = sg + (size_t)ws.stage * TG_::GROW + ls.uoff;
+    const double2 ga = *reinterpret_cast<const double2*>(grow);
+    const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
+    g0[0] = ga.x; g0[1] = ga.y; g0[2] = gb.x; g0[3] = gb.y;
+    __syncwarp();
+    if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * ws.stage);
+    if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
+    const double cc[4] = {c01.x, c01.y, c23.x, c23.y};
+    push_row<R, K>(ws, 0, ph, cc, l2, l1, r1, r2);
+  }
+  // ---- levels, in order; level l hands its row to level l+1 in registers
+#pragma unroll
+  for (int l = 0; l < K; ++l) {
+    double g[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[j] = (l == 0) ? g0[j] : ws.gr[l][(ph + P - R) % P][j];
+    if (l + 1 < K) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ws.gr[l + 1][ph][j] = g[j];
+    }
+    const int G = ls.row_base + kk - (l + 1) * R;           // global row of the output
+    const bool rowin = (unsigned)G < (unsigned)p.rows;
+    double o[4], dd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double uw[P], x1[P], x2[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {                      // logical row q -> ring slot
+        const int sl = (ph + 1 + q) % P;
+        uw[q] = ws.u[l][sl][j];
+        x1[q] = ws.h1[l][sl][j];
+        x2[q] = ws.h2[l][sl][j];
+      }
+      const double J = Point<STENCIL>::jacobi_target(uw, x1, x2, g[j]);
+      dd[j] = __dsub_rn(J, uw[R]);
+      o[j] = (FAST || (rowin && ls.in[j])) ? __fma_rn(ws.wl[l], dd[j], uw[R]) : uw[R];
+    }
+    const bool active = kk >= 2 * (l + 1) * R;
+    if (REDUCE && l == 0 && active && (unsigned)(G - ls.ja) < (unsigned)(ls.jb - ls.ja)) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (ls.own[j]) { acc_s = __fma_rn(dd[j], dd[j], acc_s); acc_m = nan_max(acc_m, fabs(dd[j])); }
+    }
+    if (l + 1 < K) {
+      // neighbours of this lane's columns at level l: adjacent lanes (the two
+      // warp-edge lanes get their own values: garbage inside the lost halo)
+      const double l1 = __shfl_up_sync(0xffffffffu, o[3], 1);
+      const double r1 = __shfl_down_sync(0xffffffffu, o[0], 1);
+      double l2 = 0.0, r2 = 0.0;
+      if (R == 2) {
+        l2 = __shfl_up_sync(0xffffffffu, o[2], 1);
+        r2 = __shfl_down_sync(0xffffffffu, o[1], 1);
+      }
+      push_row<R, K>(ws, l + 1, ph, o, l2, l1, r1, r2);
+    } else if (active) {
+      if (STORE) {
+        // FAST: every column is interior, ownership depends on the lane only
+        // (E even: both columns of a pair are owned or neither)
+        const bool own01 = FAST ? (4 * lane >= E && 4 * lane + 2 <= WG::WSPAN - E)
+                                : (ls.own[0] && ls.own[1]);
+        const bool own23 = FAST ? (4 * lane + 2 >= E && 4 * lane + 4 <= WG::WSPAN - E)
+                                : (ls.own[2] && ls.own[3]);
+        if (own01) *reinterpret_cast<double2*>(ls.outp) = make_double2(o[0], o[1]);
+        else if (!FAST) {
+          if (ls.own[0]) ls.outp[0] = o[0];
+          if (ls.own[1]) ls.outp[1] = o[1];
+        }
+        if (own23) *reinterpret_cast<double2*>(ls.outp + 2) = make_double2(o[2], o[3]);
+        else if (!FAST) {
+          if (ls.own[2]) ls.outp[2] = o[2];
+          if (ls.own[3]) ls.outp[3] = o[3];
+        }
+      }
+      ls.outp += p.ld;
+    }
+  }
+}
+
 template <int STENCIL, int NW, int K, bool REDUCE, bool STORE, bool FAST>
 __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws,
                                              const SweepParams& p, const double* su,
@@ -80,126 +194,43 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws
   constexpr int R = Point<STENCIL>::R;
   constexpr int P = 2 * R + 1;
   using WG = WarpGeom<R, K>;
-  using TG_ = TileV4<R, K, NW>;
   constexpr int E = WG::E;
-  const long long ld = p.ld;
-  const int rows = p.rows;
   const int wbase = warp * WG::WOUT;                 // warp window offset in the tile
-  const int cw = c0 + wbase;                         // first column of the warp window
-  const int cl = cw + 4 * lane;                      // first column of this lane
-  bool in[4], own[4];
+  const int cl = c0 + wbase + 4 * lane;              // first column of this lane
+  LaneSeg ls;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int c = cl + j;
-    in[j] = c >= 0 && c < p.nx;
-    own[j] = in[j] && (4 * lane + j) >= E && (4 * lane + j) < WG::WSPAN - E;
+    ls.in[j] = c >= 0 && c < p.nx;
+    ls.own[j] = ls.in[j] && (4 * lane + j) >= E && (4 * lane + j) < WG::WSPAN - E;
   }
+  ls.ja = ja;
+  ls.jb = jb;
+  ls.row_base = ja - K * R;
+  ls.uoff = wbase + 4 * lane;                        // shared index of column cl - 2
+  ls.outp = dst + (long long)(ja + R) * p.ld + PADL + cl;
   const int nin = jb - ja + 2 * K * R;
-  const int row_base = ja - K * R;
-  double* outp = dst + (long long)(ja + R) * ld + PADL + cl;
-  const int uoff = wbase + 4 * lane;                 // shared index of column cl - 2
-
-  for (int k0 = 0; k0 < nin; k0 += P) {
-#pragma unroll
-    for (int ph = 0; ph < P; ++ph) {
-      const int kk = k0 + ph;
-      if (kk < nin) {
-        // ---- level 0 input: the TMA row of step kk
-        double g0[4] = {0.0, 0.0, 0.0, 0.0};
-        {
-          mbar_wait_a(ws.full_a + 8u * ws.stage, ws.phase);
-          const double* row = su + (size_t)ws.stage * TG_::ROW + uoff;
-          const double2 c01 = *reinterpret_cast<const double2*>(row + 2);
-          const double2 c23 = *reinterpret_cast<const double2*>(row + 4);
-          double l2 = 0.0, l1, r1, r2 = 0.0;
-          if (R == 2) {
-            const double2 lft = *reinterpret_cast<const double2*>(row);
-            const double2 rgt = *reinterpret_cast<const double2*>(row + 6);
-            l2 = lft.x; l1 = lft.y; r1 = rgt.x; r2 = rgt.y;
-          } else {
-            l1 = row[1];
-            r1 = row[6];
-          }
-          if (kk >= 2 * R) {
-            const double* grow = sg + (size_t)ws.stage * TG_::GROW + uoff;
-            const double2 ga = *reinterpret_cast<const double2*>(grow);
-            const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
-            g0[0] = ga.x; g0[1] = ga.y; g0[2] = gb.x; g0[3] = gb.y;
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * ws.stage);
-          if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
-          const double cc[4] = {c01.x, c01.y, c23.x, c23.y};
-          push_row<R, K>(ws, 0, ph, cc, l2, l1, r1, r2);
-        }
-        // ---- levels, in order; level l hands its row to level l+1 in registers
-#pragma unroll
-        for (int l = 0; l < K; ++l) {
-          double g[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) g[j] = (l == 0) ? g0[j] : ws.gr[l][(ph + P - R) % P][j];
-          if (l + 1 < K) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) ws.gr[l + 1][ph][j] = g[j];
-          }
-          if (kk >= 2 * (l + 1) * R) {
-            const int G = row_base + kk - (l + 1) * R;           // global row of the output
-            const bool rowin = (unsigned)G < (unsigned)rows;
-            double o[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              double uw[P], x1[P], x2[P];
-#pragma unroll
-              for (int q = 0; q < P; ++q) {                      // logical row q -> slot
-                const int sl = (ph + 1 + q) % P;
-                uw[q] = ws.u[l][sl][j];
-                x1[q] = ws.h1[l][sl][j];
-                x2[q] = ws.h2[l][sl][j];
-              }
-              const double J = Point<STENCIL>::jacobi_target(uw, x1, x2, g[j]);
-              const double d = __dsub_rn(J, uw[R]);
-              o[j] = (FAST || (rowin && in[j])) ? __fma_rn(ws.wl[l], d, uw[R]) : uw[R];
-              if (REDUCE && l == 0 && (unsigned)(G - ja) < (unsigned)(jb - ja) && own[j]) {
-                acc_s = __fma_rn(d, d, acc_s);
-                acc_m = nan_max(acc_m, fabs(d));
-              }
-            }
-            if (l + 1 < K) {
-              // neighbours of this lane's columns at level l: adjacent lanes
-              const double l1 = __shfl_up_sync(0xffffffffu, o[3], 1);
-              const double r1 = __shfl_down_sync(0xffffffffu, o[0], 1);
-              double l2 = 0.0, r2 = 0.0;
-              if (R == 2) {
-                l2 = __shfl_up_sync(0xffffffffu, o[2], 1);
-                r2 = __shfl_down_sync(0xffffffffu, o[1], 1);
-              }
-              push_row<R, K>(ws, l + 1, ph, o, l2, l1, r1, r2);
-            } else {
-              if (STORE) {
-                // FAST: every column is interior, ownership depends on the lane only
-                // (E even: both columns of a pair are owned or neither)
-                const bool own01 = FAST ? (4 * lane >= E && 4 * lane + 2 <= WG::WSPAN - E)
-                                        : (own[0] && own[1]);
-                const bool own23 = FAST ? (4 * lane + 2 >= E && 4 * lane + 4 <= WG::WSPAN - E)
-                                        : (own[2] && own[3]);
-                if (own01) *reinterpret_cast<double2*>(outp) = make_double2(o[0], o[1]);
-                else if (!FAST) {
-                  if (own[0]) outp[0] = o[0];
-                  if (own[1]) outp[1] = o[1];
-                }
-                if (own23) *reinterpret_cast<double2*>(outp + 2) = make_double2(o[2], o[3]);
-                else if (!FAST) {
-                  if (own[2]) outp[2] = o[2];
-                  if (own[3]) outp[3] = o[3];
-                }
-              }
-              outp += ld;
-            }
-          }
-        }
-      }
+  if (c0 + wbase >= p.nx + R) {
+    // the whole warp window lies right of the last ghost column (ragged last
+    // strip): nothing to compute, keep the TMA ring in step
+    for (int kk = 0; kk < nin; ++kk) {
+      mbar_wait_a(ws.full_a + 8u * ws.stage, ws.phase);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * ws.stage);
+      if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
     }
+    return;
   }
+  int k0 = 0;
+  for (; k0 + P <= nin; k0 += P) {                  // full periods: no guards
+#pragma unroll
+    for (int ph = 0; ph < P; ++ph)
+      warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s, acc_m);
+  }
+#pragma unroll
+  for (int ph = 0; ph < P - 1; ++ph)                 // tail
+    if (k0 + ph < nin)
+      warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s, acc_m);
 }
 
 template <int STENCIL, int NW, int K, bool REDUCE, bool STORE>
