@@ -105,6 +105,9 @@ typedef struct {
     int ctas_per_sm;       /* resident CTAs per SM of the persistent sweep grid */
     int stages;            /* depth of the TMA row ring */
     int graph_chunk;       /* sweeps captured per CUDA graph */
+    int band_split;        /* 1: run every K=1 hot sweep as boundary-band launches +
+                              interior launch (the multi-GPU overlap schedule) even
+                              without NCCL; for tests */
 } cjm_options;
 
 typedef struct {

@@ -48,7 +48,8 @@ class Options(C.Structure):
                 ("nccl_id", C.c_void_p), ("device", C.c_int), ("external_halo", C.c_int),
                 ("temporal_k", C.c_int), ("variant", C.c_int),
                 ("tile_w", C.c_int),
-                ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int)]
+                ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int),
+                ("band_split", C.c_int)]
 
 
 class HaloMsg(C.Structure):

@@ -164,7 +164,10 @@ struct cjm_plan_s {
   // launch configuration
   int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
   int variant = 4;   // 3: shared-line levels (sweep.cuh), 4: warp-tiled (sweep_v4.cuh)
+  int band_split = 0;  // split hot sweeps into boundary / interior bands even without NCCL
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t comm_stream = nullptr;               // multi-GPU halo exchange
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::map<std::pair<long long, int>, cudaGraphExec_t> graphs;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double plan_s = 0;
@@ -203,7 +206,13 @@ size_t smem_bytes(const cjm_plan_s* pl, int K) {
 int block_threads(const cjm_plan_s* pl) { return pl->variant == 4 ? 4 * 32 + 32 : pl->NT + 32; }
 
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur.
-cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
+// One sweep-kernel launch of K fused sweeps reading buffer host_cur, over the
+// output rows [row0, row0 + nrows) of the slab (default: all of them).  Only
+// a launch with advance = 1 moves the device-side n / cur (the last launch of
+// a sweep that is split into bands).
+cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int row0 = 0,
+                        int nrows = -1, int advance = 1) {
+  if (nrows < 0) nrows = pl->ny_local;
   cjm::SweepParams sp;
   sp.buf[0] = pl->buf[0];
   sp.buf[1] = pl->buf[1];
@@ -216,15 +225,19 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
   sp.ld = pl->ld;
   sp.nx = pl->nx;
   sp.rows = pl->ny_local;
+  sp.row0 = row0;
+  sp.nrows = nrows;
   sp.stages = pl->stages;
+  sp.advance = advance;
   const int tout = tile_out(pl, K);
   const long long nstrips = (pl->nx + tout - 1) / tout;
-  sp.units = nstrips * pl->ny_local;
+  sp.units = nstrips * nrows;
+  const int grid = (int)std::min<long long>(pl->nctas, sp.units);
   KernelFn k = pick_kernel(pl->stencil, pl->variant, pl->NT, K, mode);
-  k<<<pl->nctas, block_threads(pl), smem_bytes(pl, K), st>>>(sp);
+  k<<<grid, block_threads(pl), smem_bytes(pl, K), st>>>(sp);
   CUDA_TRY(cudaGetLastError());
   pl->launches += 1;
-  if (mode != MODE_RESID) pl->host_cur ^= 1;
+  if (mode != MODE_RESID && advance) pl->host_cur ^= 1;
   return CJM_OK;
 }
 
@@ -250,7 +263,27 @@ cjm_status halo_exchange(cjm_plan_s* pl, double* b, cudaStream_t st) {
 }
 
 // A sweep launch followed by the halo exchange of its output (multi-GPU).
+// Hot sweeps with a communicator overlap the exchange with the interior
+// (SURVEY 8(e)): the 2r boundary rows are computed first (two small band
+// launches), the NCCL exchange of those rows runs on the plan's comm stream
+// while the interior band runs on the main stream, and the main stream waits
+// for the exchange before the next sweep.  The interior launch is the one
+// that advances n / cur.  Check sweeps (the reduction must cover every row of
+// one launch) are not split.
 cjm_status sweep_and_exchange(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
+  const int R = pl->R, nyl = pl->ny_local;
+  if (mode == MODE_HOT && (pl->comm || pl->band_split) && K == 1 && nyl > 4 * R) {
+    STATUS_TRY(launch_sweep(pl, mode, K, st, 0, R, 0));
+    STATUS_TRY(launch_sweep(pl, mode, K, st, nyl - R, R, 0));
+    double* out = pl->buf[pl->host_cur ^ 1];    // the buffer this sweep writes
+    CUDA_TRY(cudaEventRecord(pl->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(pl->comm_stream, pl->ev_fork, 0));
+    STATUS_TRY(halo_exchange(pl, out, pl->comm_stream));
+    CUDA_TRY(cudaEventRecord(pl->ev_join, pl->comm_stream));
+    STATUS_TRY(launch_sweep(pl, mode, K, st, R, nyl - 2 * R, 1));
+    CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_join, 0));
+    return CJM_OK;
+  }
   STATUS_TRY(launch_sweep(pl, mode, K, st));
   return halo_exchange(pl, pl->buf[pl->host_cur], st);
 }
@@ -599,6 +632,9 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   p->graphs.clear();
   for (auto& e : p->ev) if (e) cudaEventDestroy(e);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   cjm::pool_free(p->device, p->buf_elems * sizeof(double), p->buf[0]);
   cjm::pool_free(p->device, p->buf_elems * sizeof(double), p->buf[1]);
   cjm::pool_free(p->device, p->g_elems * sizeof(double), p->G);
@@ -695,11 +731,14 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   // ---- launch configuration
   // defaults from the r01 tuning sweep on B200 (profiles/r01_v3b_tune.jsonl):
   // two sweeps fused per launch, 256-column tiles, 4-row TMA ring, 4 CTAs/SM
-  pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 4;
+  // multi-GPU: one CTA slot per SM left free so the NCCL exchange kernels can
+  // run next to the persistent interior kernel
+  pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : (opt.world_size > 1 ? 3 : 4);
   pl->NT = opt.tile_w == 512 ? 256 : 128;
   // warp-tiled (4) by default; the 17-point with K >= 2 needs the shared-line
   // variant (3), whose per-thread state is half as large
   pl->variant = opt.variant ? opt.variant : 4;
+  pl->band_split = opt.band_split;
   pl->K = opt.temporal_k > 0 ? opt.temporal_k : 2;
   if (pl->world > 1) pl->K = 1;   // deep halos for K > 1 across ranks: not implemented
   if (stencil == 17 && pl->K > 1) {
@@ -756,6 +795,9 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   PLAN_CUDA(cudaMemset(pl->state, 0, sizeof(cjm::SweepState)));
   PLAN_CUDA(cudaMallocHost(&pl->result_host, 2 * sizeof(double)));
   PLAN_CUDA(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
+  PLAN_CUDA(cudaStreamCreateWithFlags(&pl->comm_stream, cudaStreamNonBlocking));
+  PLAN_CUDA(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming));
+  PLAN_CUDA(cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming));
   for (auto& e : pl->ev) PLAN_CUDA(cudaEventCreate(&e));
 
   if (pl->world > 1 && !opt.external_halo) {

@@ -57,10 +57,12 @@ struct SweepParams {
   double* result;              // sum d^2, max |d| (REDUCE)
   long long P;                 // weights per cycle
   long long ld;                // pitch of every internal buffer, doubles
-  long long units;             // nstrips * rows
+  long long units;             // nstrips * nrows
   int nx;                      // interior columns
-  int rows;                    // interior rows of this (slab) buffer
+  int rows;                    // interior rows of this (slab) buffer (ghost test)
+  int row0, nrows;             // the band of output rows of this launch
   int stages;                  // TMA ring depth
+  int advance;                 // the last CTA advances n / flips cur (last launch of a sweep)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -466,9 +468,9 @@ cjm_sweep_kernel(const SweepParams p) {
       uint32_t phase = 0;
       long long used = 0;
       for (long long uu = u_begin; uu < u_end;) {
-        const int strip = (int)(uu / rows);
-        const int ja = (int)(uu - (long long)strip * rows);
-        const long long seg_end = min(u_end, (long long)(strip + 1) * rows);
+        const int strip = (int)(uu / p.nrows);
+        const int ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
+        const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
         const int jb = ja + (int)(seg_end - uu);
         const int c0 = strip * TOUT - E;
         // u columns [c0-2, min(c0+T+2, nx+R+2)), g columns [c0, min(c0+T, nx))
@@ -503,9 +505,9 @@ cjm_sweep_kernel(const SweepParams p) {
     ConsumerState<R, K> cs;
     cs.init(p, n, full, empty);
     for (long long uu = u_begin; uu < u_end;) {
-      const int strip = (int)(uu / rows);
-      const int ja = (int)(uu - (long long)strip * rows);
-      const long long seg_end = min(u_end, (long long)(strip + 1) * rows);
+      const int strip = (int)(uu / p.nrows);
+      const int ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
+      const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
       const int jb = ja + (int)(seg_end - uu);
       const int c0 = strip * TOUT - E;
       // FAST: every row the segment touches is interior and the tile holds no
@@ -572,7 +574,7 @@ cjm_sweep_kernel(const SweepParams p) {
       }
     }
     if (tid == 0) {
-      if (STORE) {
+      if (STORE && p.advance) {
         p.state->n = n + (unsigned long long)K;
         p.state->cur = cur ^ 1u;
       }

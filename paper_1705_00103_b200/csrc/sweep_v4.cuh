@@ -283,9 +283,9 @@ cjm_sweep_kernel_v4(const SweepParams p) {
       long long used = 0;
       const uint32_t full_a = smem_addr(full), empty_a = smem_addr(empty);
       for (long long uu = u_begin; uu < u_end;) {
-        const int strip = (int)(uu / rows);
-        const int ja = (int)(uu - (long long)strip * rows);
-        const long long seg_end = min(u_end, (long long)(strip + 1) * rows);
+        const int strip = (int)(uu / p.nrows);
+        const int ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
+        const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
         const int jb = ja + (int)(seg_end - uu);
         const int c0 = strip * TG_::TOUT - E;
         const int ucols = min(TG_::TLOAD, p.nx + R + 2 - c0);
@@ -329,9 +329,9 @@ cjm_sweep_kernel_v4(const SweepParams p) {
     ws.full_a = smem_addr(full);
     ws.empty_a = smem_addr(empty);
     for (long long uu = u_begin; uu < u_end;) {
-      const int strip = (int)(uu / rows);
-      const int ja = (int)(uu - (long long)strip * rows);
-      const long long seg_end = min(u_end, (long long)(strip + 1) * rows);
+      const int strip = (int)(uu / p.nrows);
+      const int ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
+      const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
       const int jb = ja + (int)(seg_end - uu);
       const int c0 = strip * TG_::TOUT - E;
       const bool fast = ja - K * R >= 0 && jb + K * R <= rows && c0 >= 0 && c0 + TG_::TG <= p.nx;
@@ -395,7 +395,7 @@ cjm_sweep_kernel_v4(const SweepParams p) {
       }
     }
     if (tid == 0) {
-      if (STORE) {
+      if (STORE && p.advance) {
         p.state->n = n + (unsigned long long)K;
         p.state->cur = cur ^ 1u;
       }

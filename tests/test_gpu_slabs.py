@@ -27,21 +27,29 @@ from paper_1705_00103_b200 import cjm  # noqa: E402
 
 @pytest.mark.parametrize("world,stencil,nx,ny", [(2, 9, 300, 257), (4, 17, 130, 97), (3, 5, 64, 200),
                                                  (8, 9, 513, 64)])
-def test_slabs_bitwise_equal_single_domain(world, stencil, nx, ny):
+@pytest.mark.parametrize("band_split", (0, 1))
+def test_slabs_bitwise_equal_single_domain(world, stencil, nx, ny, band_split):
+    """band_split=1 runs each sweep as the multi-GPU overlap schedule does:
+    boundary-row bands first, then the interior band (which advances n)."""
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=21)
     nsweeps = 9
     plans, us, bs, msgs = [], [], [], []
     for g in range(world):
         y0, nyl = cjm.cjm_slab(ny, world, g)
-        plans.append(cjm.Plan(stencil, nx, ny, h, 1e-8, world_size=world, rank=g, external_halo=1))
+        plans.append(cjm.Plan(stencil, nx, ny, h, 1e-8, world_size=world, rank=g, external_halo=1,
+                              band_split=band_split))
         assert (plans[-1].y0, plans[-1].ny_local) == (y0, nyl)
         us.append(torch.from_numpy(u0[y0:y0 + nyl + 2 * r].copy()).cuda())
         bs.append(torch.from_numpy(b[y0:y0 + nyl].copy()).cuda())
         msgs.append(cjm.cjm_halo_plan(ny, r, world, g))
     for k in range(nsweeps):
         for g in range(world):
-            plans[g].sweeps(bs[g], us[g], k, 1)
+            rep = plans[g].sweeps(bs[g], us[g], k, 1)
+            if band_split and plans[g].ny_local > 4 * r:
+                assert rep["kernel_launches"] >= 5     # 3 band launches + setup
+            else:
+                assert rep["kernel_launches"] >= 3
         staged = []
         for g in range(world):                       # read every send block first
             for m in msgs[g]:
