@@ -169,6 +169,7 @@ struct cjm_plan_s {
   cudaStream_t comm_stream = nullptr;               // multi-GPU halo exchange
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::map<std::pair<long long, int>, cudaGraphExec_t> graphs;
+  std::map<std::pair<long long, int>, long long> graph_kernels;   // kernels per graph
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double plan_s = 0;
   // host mirror of the device state during a call
@@ -291,11 +292,16 @@ cjm_status sweep_and_exchange(cjm_plan_s* pl, int mode, int K, cudaStream_t st) 
 // Graph of `len` hot launches of K sweeps each.  Single GPU: every launch has
 // identical parameters (buffers resolved on the device), one graph per length.
 // Multi-GPU: the NCCL buffers depend on the starting buffer parity.
-cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out) {
+cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out,
+                     long long* kernels) {
   const int par = pl->world > 1 ? pl->host_cur : 0;
   const std::pair<long long, int> key{len * 8 + K, par};
   auto it = pl->graphs.find(key);
-  if (it != pl->graphs.end()) { *out = it->second; return CJM_OK; }
+  if (it != pl->graphs.end()) {
+    *out = it->second;
+    *kernels = pl->graph_kernels[key];
+    return CJM_OK;
+  }
   const int saved_cur = pl->host_cur;
   const long long saved_launches = pl->launches;
   cudaGraph_t graph = nullptr;
@@ -304,6 +310,7 @@ cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out)
   for (long long k = 0; k < len && s == CJM_OK; ++k) s = sweep_and_exchange(pl, MODE_HOT, K, pl->cap_stream);
   cudaError_t e = cudaStreamEndCapture(pl->cap_stream, &graph);
   pl->host_cur = saved_cur;
+  const long long captured = pl->launches - saved_launches;
   pl->launches = saved_launches;
   if (s != CJM_OK) { if (graph) cudaGraphDestroy(graph); return s; }
   CUDA_TRY(e);
@@ -312,7 +319,9 @@ cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out)
   cudaGraphDestroy(graph);
   CUDA_TRY(e);
   pl->graphs[key] = exec;
+  pl->graph_kernels[key] = captured;
   *out = exec;
+  *kernels = captured;
   return CJM_OK;
 }
 
@@ -325,10 +334,11 @@ cjm_status run_hot(cjm_plan_s* pl, long long count, cudaStream_t st, long long* 
   while (blocks > 0) {
     const long long len = std::min<long long>(pl->graph_chunk, blocks);
     cudaGraphExec_t ex;
-    STATUS_TRY(get_graph(pl, len, K, &ex));
+    long long kernels = 0;
+    STATUS_TRY(get_graph(pl, len, K, &ex, &kernels));
     CUDA_TRY(cudaGraphLaunch(ex, st));
     pl->host_cur ^= (int)(len & 1);
-    pl->launches += len;
+    pl->launches += kernels;
     *hot_launches += len;
     blocks -= len;
   }
@@ -630,6 +640,7 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   cudaDeviceSynchronize();
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   p->graphs.clear();
+  p->graph_kernels.clear();
   for (auto& e : p->ev) if (e) cudaEventDestroy(e);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
