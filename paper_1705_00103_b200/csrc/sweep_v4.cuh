@@ -334,7 +334,10 @@ cjm_sweep_kernel_v4(const SweepParams p) {
       const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
       const int jb = ja + (int)(seg_end - uu);
       const int c0 = strip * TG_::TOUT - E;
-      const bool fast = ja - K * R >= 0 && jb + K * R <= rows && c0 >= 0 && c0 + TG_::TG <= p.nx;
+      // FAST per warp: its window holds no ghost / padding column and the
+      // segment touches no ghost row
+      const int cw = c0 + warp * WG::WOUT;
+      const bool fast = ja - K * R >= 0 && jb + K * R <= rows && cw >= 0 && cw + WG::WSPAN <= p.nx;
       if (fast)
         warp_segment<STENCIL, NW, K, REDUCE, STORE, true>(ws, p, su, sg, dst, ja, jb, c0, warp, lane,
                                                           acc_s, acc_m);
