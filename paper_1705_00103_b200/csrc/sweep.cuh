@@ -100,14 +100,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done) : "r"(a), "r"(parity) : "memory");
-  } while (!done);
+  // the retry loop lives inside the asm block: no C-level divergent loop, so
+  // the compiler emits no convergence barrier around it
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "CJM_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra CJM_WAIT_%=;\n\t}"
+      ::"r"(a), "r"(parity) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
