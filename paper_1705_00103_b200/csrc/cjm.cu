@@ -765,6 +765,12 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   // resident).  Check / residual / remainder kernels may need more registers;
   // they then run the same grid in more than one wave, which is correct
   // because no CTA ever waits for another.
+  int smem_optin = 0;
+  PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (smem_bytes(pl, pl->K) > (size_t)smem_optin - 2048) {
+    set_error("cjm_plan", "TMA ring too deep for shared memory (lower stages)");
+    return fail(CJM_ERR_INVALID_ARG);
+  }
   int occ_min = 1 << 30;
   for (int K = 1; K <= pl->K; ++K) {
     if (K != 1 && K != pl->K) continue;

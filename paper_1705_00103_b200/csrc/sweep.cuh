@@ -110,6 +110,12 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
       ::"r"(a), "r"(parity) : "memory");
 }
 
+// Order this thread's generic-proxy reads of a ring slot before the async-proxy
+// (TMA) writes that will refill it once the slot is released (cross-proxy WAR).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
@@ -335,6 +341,7 @@ __device__ __forceinline__ void consumer_segment(ConsumerState<Point<STENCIL>::R
                 g0a = gv.x;
                 g0b = gv.y;
               }
+              fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) mbar_arrive_a(cs.empty_a + 8u * cs.stage);
               if (++cs.stage == p.stages) { cs.stage = 0; cs.phase ^= 1u; }

@@ -111,7 +111,9 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
     const double2 ga = *reinterpret_cast<const double2*>(grow);
     const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
     g0[0] = ga.x; g0[1] = ga.y; g0[2] = gb.x; g0[3] = gb.y;
-    mbar_arrive_a(ws.empty_a + 8u * ws.stage);     // every lane, after its own reads
+    fence_proxy_async_smem();   // my reads of the slot before its TMA refill
+    __syncwarp();
+    if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * ws.stage);
     if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
     const double cc[4] = {c01.x, c01.y, c23.x, c23.y};
     push_row<R, K>(ws, 0, ph, cc, l2, l1, r1, r2);
@@ -214,7 +216,8 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws
     // strip): nothing to compute, keep the TMA ring in step
     for (int kk = 0; kk < nin; ++kk) {
       mbar_wait_a(ws.full_a + 8u * ws.stage, ws.phase);
-      mbar_arrive_a(ws.empty_a + 8u * ws.stage);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * ws.stage);
       if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
     }
     return;
@@ -255,7 +258,7 @@ cjm_sweep_kernel_v4(const SweepParams p) {
   if (tid == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 32 * NW);   // every consumer lane arrives
+      mbar_init(&empty[s], NW);        // one arrival per consumer warp
     }
     fence_mbar_init();
   }

@@ -1,0 +1,36 @@
+"""Repeated-run stress test of the TMA ring (slot reuse across the generic
+and async proxies).  A shallow ring (2 stages) and the cheapest consumer
+(variant 4, K = 1) make a missing cross-proxy fence show up as a
+non-deterministic wrong value within a few dozen runs (it did: 35 of 200 runs
+before fence.proxy.async was added).  Every run must equal the oracle."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1705_00103_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1705_00103_b200 import cjm  # noqa: E402
+
+
+@pytest.mark.parametrize("variant,K,stages", [(4, 1, 2), (4, 2, 2), (3, 1, 2), (4, 1, 4)])
+def test_ring_reuse_is_race_free(variant, K, stages):
+    n, cnt, trials = 1024, 16, 60
+    u0, b, h = inputs.test_problem(n, n, 1, init="random")
+    s = oracle.schedule(5, n, n, 1e-8)
+    ref = oracle.sweeps(5, u0, oracle.rhs_to_g(5, h, b), s["w"], 0, cnt)
+    bd = torch.from_numpy(b).cuda()
+    bad = 0
+    with cjm.Plan(5, n, n, h, 1e-8, temporal_k=K, variant=variant, stages=stages) as plan:
+        for _ in range(trials):
+            ud = torch.from_numpy(u0.copy()).cuda()
+            plan.sweeps(bd, ud, 0, cnt)
+            bad += not np.array_equal(ud.cpu().numpy(), ref)
+    assert bad == 0, f"{bad} of {trials} runs differ from the oracle"
