@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -30,6 +31,28 @@
 namespace {
 
 thread_local std::string g_last_error;
+
+// CJM_TRACE=1 in the environment: host-side phase timings on stderr
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("CJM_TRACE");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
+struct TraceTimer {
+  const char* scope;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit TraceTimer(const char* s) : scope(s) {}
+  void mark(const char* what) {
+    if (!trace_on()) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cjm] %s %-24s %9.3f ms\n", scope, what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 void set_error(const char* what, const char* msg) {
   g_last_error = std::string(what) + ": " + msg;
@@ -161,6 +184,8 @@ struct cjm_plan_s {
   double* result_host = nullptr;  // pinned, 2 doubles
   cjm::SweepState* state = nullptr;
   unsigned long long* err_bits = nullptr;   // real-error reduction (cjm_solve_ref)
+  void* small_block = nullptr;              // partials | result | state | err_bits
+  size_t small_bytes = 0;
   // launch configuration
   int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
   int variant = 4;   // 3: shared-line levels (sweep.cuh), 4: warp-tiled (sweep_v4.cuh)
@@ -304,6 +329,7 @@ cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out,
   }
   const int saved_cur = pl->host_cur;
   const long long saved_launches = pl->launches;
+  TraceTimer tt("graph");
   cudaGraph_t graph = nullptr;
   CUDA_TRY(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
   cjm_status s = CJM_OK;
@@ -320,6 +346,7 @@ cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out,
   CUDA_TRY(e);
   pl->graphs[key] = exec;
   pl->graph_kernels[key] = captured;
+  tt.mark("capture+instantiate");
   *out = exec;
   *kernels = captured;
   return CJM_OK;
@@ -636,11 +663,14 @@ cjm_status cjm_get_nccl_id(void* out128) {
 
 cjm_status cjm_plan_destroy(cjm_plan_t p) {
   if (!p) return CJM_OK;
+  TraceTimer tt("destroy");
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
+  tt.mark("device sync");
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   p->graphs.clear();
   p->graph_kernels.clear();
+  tt.mark("graph exec destroy");
   for (auto& e : p->ev) if (e) cudaEventDestroy(e);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
@@ -649,13 +679,11 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   cjm::pool_free(p->device, p->buf_elems * sizeof(double), p->buf[0]);
   cjm::pool_free(p->device, p->buf_elems * sizeof(double), p->buf[1]);
   cjm::pool_free(p->device, p->g_elems * sizeof(double), p->G);
-  cudaFree(p->w_dev);
-  cudaFree(p->partials);
-  cudaFree(p->result);
-  cudaFree(p->state);
-  cudaFree(p->err_bits);
-  if (p->result_host) cudaFreeHost(p->result_host);
+  cjm::pool_free(p->device, (size_t)p->P * sizeof(double), p->w_dev);
+  cjm::pool_free(p->device, p->small_bytes, p->small_block);
+  cjm::pool_free_host(2 * sizeof(double), p->result_host);
   if (p->comm) ncclCommDestroy(p->comm);
+  tt.mark("free");
   delete p;
   return CJM_OK;
 }
@@ -732,6 +760,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
     }                                                                    \
   } while (0)
 
+  TraceTimer tt("plan");
   int dev = opt.device;
   if (dev < 0) PLAN_CUDA(cudaGetDevice(&dev));
   pl->device = dev;
@@ -759,7 +788,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
     }
     pl->variant = 3;
   }
-  pl->stages = opt.stages > 0 ? opt.stages : 4;
+  pl->stages = opt.stages > 0 ? opt.stages : (pl->variant == 4 ? 8 : 4);
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
   // The grid is sized for the hot kernel (persistent: ctas_per_sm per SM, all
   // resident).  Check / residual / remainder kernels may need more registers;
@@ -792,6 +821,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   }
   pl->nctas = nsm * std::min(occ_min, pl->ctas_per_sm);
 
+  tt.mark("schedule+config");
   // ---- buffers: (ny_local + 2R) rows of pitch ld; interior column 0 at PADL
   pl->ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
   pl->buf_elems = (size_t)(nyl + 2 * R) * pl->ld;
@@ -802,15 +832,21 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   PLAN_CUDA(cudaMemset(pl->buf[0], 0, pl->buf_elems * sizeof(double)));
   PLAN_CUDA(cudaMemset(pl->buf[1], 0, pl->buf_elems * sizeof(double)));
   PLAN_CUDA(cudaMemset(pl->G, 0, pl->g_elems * sizeof(double)));
-  PLAN_CUDA(cudaMalloc(&pl->w_dev, (size_t)pl->P * sizeof(double)));
+  tt.mark("field buffers");
+  PLAN_CUDA(cjm::pool_alloc(dev, (size_t)pl->P * sizeof(double), (void**)&pl->w_dev));
   PLAN_CUDA(cudaMemcpy(pl->w_dev, pl->sched.w.data(), (size_t)pl->P * sizeof(double),
                        cudaMemcpyHostToDevice));
-  PLAN_CUDA(cudaMalloc(&pl->partials, (size_t)pl->nctas * 2 * sizeof(double)));
-  PLAN_CUDA(cudaMalloc(&pl->result, 2 * sizeof(double)));
-  PLAN_CUDA(cudaMalloc(&pl->state, sizeof(cjm::SweepState)));
-  PLAN_CUDA(cudaMalloc(&pl->err_bits, sizeof(unsigned long long)));
+  // one small block: partials (2 per CTA), result (2), state, real-error bits
+  pl->small_bytes = ((size_t)pl->nctas * 2 + 2) * sizeof(double) + sizeof(cjm::SweepState) +
+                    sizeof(unsigned long long);
+  PLAN_CUDA(cjm::pool_alloc(dev, pl->small_bytes, &pl->small_block));
+  pl->partials = static_cast<double*>(pl->small_block);
+  pl->result = pl->partials + (size_t)pl->nctas * 2;
+  pl->state = reinterpret_cast<cjm::SweepState*>(pl->result + 2);
+  pl->err_bits = reinterpret_cast<unsigned long long*>(pl->state + 1);
   PLAN_CUDA(cudaMemset(pl->state, 0, sizeof(cjm::SweepState)));
-  PLAN_CUDA(cudaMallocHost(&pl->result_host, 2 * sizeof(double)));
+  PLAN_CUDA(cjm::pool_alloc_host(2 * sizeof(double), (void**)&pl->result_host));
+  tt.mark("weights+small");
   PLAN_CUDA(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
   PLAN_CUDA(cudaStreamCreateWithFlags(&pl->comm_stream, cudaStreamNonBlocking));
   PLAN_CUDA(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming));
@@ -828,6 +864,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   }
   PLAN_CUDA(cudaDeviceSynchronize());
 #undef PLAN_CUDA
+  tt.mark("streams+nccl+sync");
   pl->plan_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = pl;
   return CJM_OK;

@@ -31,6 +31,8 @@ bool build_schedule(int stencil, int nx, int ny, double tol, int order, Schedule
 cudaError_t pool_alloc(int device, size_t bytes, void** out);
 void pool_free(int device, size_t bytes, void* p);
 void pool_trim();
+cudaError_t pool_alloc_host(size_t bytes, void** out);
+void pool_free_host(size_t bytes, void* p);
 size_t pool_cached_bytes();
 
 }  // namespace cjm

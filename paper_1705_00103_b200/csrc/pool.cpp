@@ -74,6 +74,30 @@ void pool_trim() {
   cudaSetDevice(prev);
 }
 
+// pinned host blocks (the 16-byte D2H landing zones of the reductions)
+namespace {
+std::multimap<size_t, void*> g_host_free;
+}
+
+cudaError_t pool_alloc_host(size_t bytes, void** out) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_host_free.find(bytes);
+    if (it != g_host_free.end()) {
+      *out = it->second;
+      g_host_free.erase(it);
+      return cudaSuccess;
+    }
+  }
+  return cudaMallocHost(out, bytes);
+}
+
+void pool_free_host(size_t bytes, void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_host_free.emplace(bytes, p);
+}
+
 size_t pool_cached_bytes() {
   std::lock_guard<std::mutex> lk(g_mu);
   return g_cached;
