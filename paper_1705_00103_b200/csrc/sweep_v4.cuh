@@ -45,7 +45,6 @@ struct WarpState {
   static constexpr int P = 2 * R + 1;
   static constexpr int C = WarpGeom<R, K>::CPL;
   double u[K][P][C], h1[K][P][C], h2[K][P][C];   // ring slot = step mod P
-  double gr[K][P][C];                            // g of level l-1, for level l R steps later
   double wl[K];
   int stage;
   uint32_t phase;
@@ -90,11 +89,14 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
   using WG = WarpGeom<R, K>;
   using TG_ = TileV4<R, K, NW>;
   constexpr int E = WG::E;
-  // ---- level 0 input: the TMA row of step kk
-  double g0[4];
+  // ---- level 0 input: the TMA row of step kk (slot rs)
+  // The slot of step kk stays held until level K-1 has read its g row, R(K-1)
+  // steps later (level l reads the g row that arrived with step kk - lR), so
+  // g needs no register ring.
+  const int rs = ws.stage;
   {
-    mbar_wait_a(ws.full_a + 8u * ws.stage, ws.phase);
-    const double* row = su + (size_t)ws.stage * TG_::ROW + ls.uoff;
+    mbar_wait_a(ws.full_a + 8u * rs, ws.phase);
+    const double* row = su + (size_t)rs * TG_::ROW + ls.uoff;
     const double2 c01 = *reinterpret_cast<const double2*>(row + 2);
     const double2 c23 = *reinterpret_cast<const double2*>(row + 4);
     double l2 = 0.0, l1, r1, r2 = 0.0;
@@ -106,14 +108,6 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
       l1 = row[1];
       r1 = row[6];
     }
-    // g of the level-0 output row (stale before kk = 2R: never used then)
-    const double* grow = sg + (size_t)ws.stage * TG_::GROW + ls.uoff;
-    const double2 ga = *reinterpret_cast<const double2*>(grow);
-    const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
-    g0[0] = ga.x; g0[1] = ga.y; g0[2] = gb.x; g0[3] = gb.y;
-    fence_proxy_async_smem();   // my reads of the slot before its TMA refill
-    __syncwarp();
-    if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * ws.stage);
     if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
     const double cc[4] = {c01.x, c01.y, c23.x, c23.y};
     push_row<R, K>(ws, 0, ph, cc, l2, l1, r1, r2);
@@ -121,12 +115,16 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
   // ---- levels, in order; level l hands its row to level l+1 in registers
 #pragma unroll
   for (int l = 0; l < K; ++l) {
+    // g of level l's output row: arrived with the u row of step kk - lR
+    // (stale during a level's warm-up: never stored then)
     double g[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) g[j] = (l == 0) ? g0[j] : ws.gr[l][(ph + P - R) % P][j];
-    if (l + 1 < K) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) ws.gr[l + 1][ph][j] = g[j];
+    {
+      int gs = rs - l * R;
+      if (gs < 0) gs += p.stages;
+      const double* grow = sg + (size_t)gs * TG_::GROW + ls.uoff;
+      const double2 ga = *reinterpret_cast<const double2*>(grow);
+      const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
+      g[0] = ga.x; g[1] = ga.y; g[2] = gb.x; g[3] = gb.y;
     }
     const int G = ls.row_base + kk - (l + 1) * R;           // global row of the output
     const bool rowin = (unsigned)G < (unsigned)p.rows;
@@ -184,6 +182,14 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
       ls.outp += p.ld;
     }
   }
+  // ---- release the slot whose last reader (level K-1's g) was this step
+  if (kk >= (K - 1) * R) {
+    int rel = rs - (K - 1) * R;
+    if (rel < 0) rel += p.stages;
+    fence_proxy_async_smem();   // my reads of the slot before its TMA refill
+    __syncwarp();
+    if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * rel);
+  }
 }
 
 template <int STENCIL, int NW, int K, bool REDUCE, bool STORE, bool FAST>
@@ -232,10 +238,28 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws
   for (int ph = 0; ph < P - 1; ++ph)                 // tail
     if (k0 + ph < nin)
       warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s, acc_m);
+  // the last R(K-1) slots of the segment were still held: release them
+  if (K > 1) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int i = (K - 1) * R; i > 0; --i) {
+        int rel = ws.stage - i;
+        if (rel < 0) rel += p.stages;
+        mbar_arrive_a(ws.empty_a + 8u * rel);
+      }
+    }
+  }
 }
 
+// K = 2 is register-limited to 2 CTAs (10 warps) per SM at its natural 168
+// registers; asking for 3 resident CTAs caps it at 136 (V4_MIN_BLOCKS_K2).
+#ifndef V4_MIN_BLOCKS_K2
+#define V4_MIN_BLOCKS_K2 3
+#endif
 template <int STENCIL, int NW, int K, bool REDUCE, bool STORE>
-__global__ void __launch_bounds__(32 * NW + 32)
+__global__ void __launch_bounds__(32 * NW + 32, (K == 2 ? V4_MIN_BLOCKS_K2 : 1))
 cjm_sweep_kernel_v4(const SweepParams p) {
   constexpr int R = Point<STENCIL>::R;
   using WG = WarpGeom<R, K>;
@@ -323,7 +347,7 @@ cjm_sweep_kernel_v4(const SweepParams p) {
 #pragma unroll
       for (int q = 0; q < 2 * R + 1; ++q)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ws.u[l][q][j] = ws.h1[l][q][j] = ws.h2[l][q][j] = ws.gr[l][q][j] = 0.0;
+        for (int j = 0; j < 4; ++j) ws.u[l][q][j] = ws.h1[l][q][j] = ws.h2[l][q][j] = 0.0;
     }
     ws.stage = 0;
     ws.phase = 0;
