@@ -256,7 +256,7 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws
 // K = 2 is register-limited to 2 CTAs (10 warps) per SM at its natural 168
 // registers; asking for 3 resident CTAs caps it at 136 (V4_MIN_BLOCKS_K2).
 #ifndef V4_MIN_BLOCKS_K2
-#define V4_MIN_BLOCKS_K2 3
+#define V4_MIN_BLOCKS_K2 1
 #endif
 template <int STENCIL, int NW, int K, bool REDUCE, bool STORE>
 __global__ void __launch_bounds__(32 * NW + 32, (K == 2 ? V4_MIN_BLOCKS_K2 : 1))
