@@ -41,6 +41,7 @@ CONFIGS = {
     "cjm17_8192": (17, 8192, 8192, 1e-8, "configs[3]: 17-point at 8192^2"),
     "cjm9_1024": (9, 1024, 1024, 1e-8, "configs[1]: 9-point at 1024^2"),
     "cjm5_1024": (5, 1024, 1024, 1e-8, "configs[1]: 5-point at 1024^2"),
+    "cjm17_1024": (17, 1024, 1024, 1e-8, "17-point at 1024^2 (tab:tab01 size)"),
     "cjm9_64": (9, 64, 64, 1e-8, "configs[0]: 9-point at 64^2"),
 }
 METRIC = "GLUPS (fp64 lattice updates/s) and time-to-tol vs HBM roofline"
