@@ -774,12 +774,15 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   // multi-GPU: one CTA slot per SM left free so the NCCL exchange kernels can
   // run next to the persistent interior kernel
   pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : (opt.world_size > 1 ? 3 : 4);
-  pl->NT = opt.tile_w == 512 ? 256 : 128;
-  // warp-tiled (4) by default; the 17-point with K >= 2 needs the shared-line
-  // variant (3), whose per-thread state is half as large
-  pl->variant = opt.variant ? opt.variant : 4;
+  // 5/9-point: warp-tiled kernel (4), two sweeps per launch.  17-point: one
+  // sweep per launch through the shared-line kernel with 512-column tiles
+  // (its 5-row windows make K >= 2 latency-bound: 423 vs 290 us per sweep at
+  // 8192^2, profiles/r01_tune17.jsonl).
+  const bool wide = stencil == 17;
+  pl->NT = opt.tile_w == 512 || (opt.tile_w == 0 && wide && opt.variant != 4) ? 256 : 128;
+  pl->variant = opt.variant ? opt.variant : (wide ? 3 : 4);
   pl->band_split = opt.band_split;
-  pl->K = opt.temporal_k > 0 ? opt.temporal_k : 2;
+  pl->K = opt.temporal_k > 0 ? opt.temporal_k : (wide ? 1 : 2);
   if (pl->world > 1) pl->K = 1;   // deep halos for K > 1 across ranks: not implemented
   if (stencil == 17 && pl->K > 1) {
     if (opt.variant == 4) {
@@ -788,7 +791,7 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
     }
     pl->variant = 3;
   }
-  pl->stages = opt.stages > 0 ? opt.stages : (pl->variant == 4 ? 8 : 4);
+  pl->stages = opt.stages > 0 ? opt.stages : (pl->variant == 4 ? 8 : (pl->NT == 256 ? 12 : 4));
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
   // The grid is sized for the hot kernel (persistent: ctas_per_sm per SM, all
   // resident).  Check / residual / remainder kernels may need more registers;
