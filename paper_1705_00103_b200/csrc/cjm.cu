@@ -797,9 +797,9 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   // resident).  Check / residual / remainder kernels may need more registers;
   // they then run the same grid in more than one wave, which is correct
   // because no CTA ever waits for another.
-  if (pl->variant == 4 && pl->stages < (pl->K - 1) * (R + 1) + 2) {
-    // the warp-tiled kernel holds a slot for (R+1)(K-1) steps after reading it
-    set_error("cjm_plan", "stages must be >= (r+1)(temporal_k-1) + 2 for variant 4");
+  if (pl->variant == 4 && pl->stages < (pl->K - 1) * R + 2) {
+    // the warp-tiled kernel holds a slot for R(K-1) steps after reading it
+    set_error("cjm_plan", "stages must be >= r(temporal_k-1) + 2 for variant 4");
     return fail(CJM_ERR_INVALID_ARG);
   }
   int smem_optin = 0;

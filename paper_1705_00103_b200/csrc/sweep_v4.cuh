@@ -74,110 +74,29 @@ __device__ __forceinline__ void push_row(WarpState<R, K>& ws, int l, int sl, con
 struct LaneSeg {
   bool in[4], own[4];
   int ja, jb, row_base, uoff;
-  int cslot;          // ring slot of the current step's TMA row
   double* outp;
 };
 
-// Compute one level's output row for this lane's 4 columns from the window
-// rows in ring slots (s0 + q) mod P, q = 0..2R, with the g row at `grow`.
-template <int STENCIL, int K, bool FAST>
-__device__ __forceinline__ void level_row(const WarpState<Point<STENCIL>::R, K>& ws, const LaneSeg& ls,
-                                          int l, int s0, const double* grow, bool rowin,
-                                          double (&o)[4], double (&dd)[4]) {
-  constexpr int R = Point<STENCIL>::R;
-  constexpr int P = 2 * R + 1;
-  const double2 ga = *reinterpret_cast<const double2*>(grow);
-  const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
-  const double g[4] = {ga.x, ga.y, gb.x, gb.y};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    double uw[P], x1[P], x2[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const int sl = (s0 + q) % P;
-      uw[q] = ws.u[l][sl][j];
-      x1[q] = ws.h1[l][sl][j];
-      x2[q] = ws.h2[l][sl][j];
-    }
-    const double J = Point<STENCIL>::jacobi_target(uw, x1, x2, g[j]);
-    dd[j] = __dsub_rn(J, uw[R]);
-    o[j] = (FAST || (rowin && ls.in[j])) ? __fma_rn(ws.wl[l], dd[j], uw[R]) : uw[R];
-  }
-}
-
-// Store the last level's row (owned columns only).
-template <int R, int K, bool FAST>
-__device__ __forceinline__ void store_row(const LaneSeg& ls, double* outp, int lane, const double (&o)[4]) {
-  using WG = WarpGeom<R, K>;
-  constexpr int E = WG::E;
-  // FAST: every column is interior, ownership depends on the lane only
-  // (E even: both columns of a pair are owned or neither)
-  const bool own01 = FAST ? (4 * lane >= E && 4 * lane + 2 <= WG::WSPAN - E) : (ls.own[0] && ls.own[1]);
-  const bool own23 = FAST ? (4 * lane + 2 >= E && 4 * lane + 4 <= WG::WSPAN - E) : (ls.own[2] && ls.own[3]);
-  if (own01) *reinterpret_cast<double2*>(outp) = make_double2(o[0], o[1]);
-  else if (!FAST) {
-    if (ls.own[0]) outp[0] = o[0];
-    if (ls.own[1]) outp[1] = o[1];
-  }
-  if (own23) *reinterpret_cast<double2*>(outp + 2) = make_double2(o[2], o[3]);
-  else if (!FAST) {
-    if (ls.own[2]) outp[2] = o[2];
-    if (ls.own[3]) outp[3] = o[3];
-  }
-}
-
-// Hand a level's output row to the next level's ring (slot sl): neighbours
-// come from the adjacent lanes (the warp-edge lanes get their own values,
-// garbage inside the lost halo).
-template <int R, int K>
-__device__ __forceinline__ void hand_over(WarpState<R, K>& ws, int l_next, int sl, const double (&o)[4]) {
-  const double l1 = __shfl_up_sync(0xffffffffu, o[3], 1);
-  const double r1 = __shfl_down_sync(0xffffffffu, o[0], 1);
-  double l2 = 0.0, r2 = 0.0;
-  if (R == 2) {
-    l2 = __shfl_up_sync(0xffffffffu, o[2], 1);
-    r2 = __shfl_down_sync(0xffffffffu, o[1], 1);
-  }
-  push_row<R, K>(ws, l_next, sl, o, l2, l1, r1, r2);
-}
-
-// One step kk (ring slot ph = kk mod P) of a lane.  Levels are skewed by one
-// step each: level l >= 1 works on the rows level l-1 produced up to step
-// kk-1, so the levels of a step are independent (more ILP) and they run from
-// the top level down, each reading its window before the level below pushes
-// this step's row into the same ring slot.  Level l's output row is
-// kk - (l+1)R - l; its g row arrived with the TMA row of step kk - l(R+1),
-// whose ring slot is therefore held (R+1)(K-1) steps before release.
+// One step (input row kk, ring slot ph = kk mod P) of a lane: read the TMA row,
+// run every level (unconditionally: a level computes garbage until its window
+// is full, which is never stored), store the last level when it is active.
 template <int STENCIL, int NW, int K, bool REDUCE, bool STORE, bool FAST>
 __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, LaneSeg& ls,
                                           const SweepParams& p, const double* su, const double* sg,
-                                          int kk, int ph, int nin, int lane, double& acc_s,
-                                          double& acc_m) {
+                                          int kk, int ph, int lane, double& acc_s, double& acc_m) {
   constexpr int R = Point<STENCIL>::R;
   constexpr int P = 2 * R + 1;
+  using WG = WarpGeom<R, K>;
   using TG_ = TileV4<R, K, NW>;
-  const int cs = ls.cslot;                          // ring slot of step kk's TMA row
-  // ---- levels K-1 .. 1
-#pragma unroll
-  for (int l = K - 1; l >= 1; --l) {
-    int gs = cs - l * (R + 1);
-    while (gs < 0) gs += p.stages;
-    const int G = ls.row_base + kk - (l + 1) * R - l;
-    double o[4], dd[4];
-    level_row<STENCIL, K, FAST>(ws, ls, l, ph, sg + (size_t)gs * TG_::GROW + ls.uoff,
-                                (unsigned)G < (unsigned)p.rows, o, dd);
-    const bool active = kk >= 2 * (l + 1) * R + l && kk < nin + l;
-    if (l + 1 < K) {
-      hand_over<R, K>(ws, l + 1, ph, o);
-    } else if (active) {
-      if (STORE) store_row<R, K, FAST>(ls, ls.outp, lane, o);
-      ls.outp += p.ld;
-    }
-  }
-  // ---- level 0: the TMA row of step kk
-  if (kk < nin) {
-    mbar_wait_a(ws.full_a + 8u * cs, ws.phase);
-    const double* row = su + (size_t)cs * TG_::ROW + ls.uoff;
+  constexpr int E = WG::E;
+  // ---- level 0 input: the TMA row of step kk (slot rs)
+  // The slot of step kk stays held until level K-1 has read its g row, R(K-1)
+  // steps later (level l reads the g row that arrived with step kk - lR), so
+  // g needs no register ring.
+  const int rs = ws.stage;
+  {
+    mbar_wait_a(ws.full_a + 8u * rs, ws.phase);
+    const double* row = su + (size_t)rs * TG_::ROW + ls.uoff;
     const double2 c01 = *reinterpret_cast<const double2*>(row + 2);
     const double2 c23 = *reinterpret_cast<const double2*>(row + 4);
     double l2 = 0.0, l1, r1, r2 = 0.0;
@@ -192,33 +111,85 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
     if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
     const double cc[4] = {c01.x, c01.y, c23.x, c23.y};
     push_row<R, K>(ws, 0, ph, cc, l2, l1, r1, r2);
-    const int G = ls.row_base + kk - R;
+  }
+  // ---- levels, in order; level l hands its row to level l+1 in registers
+#pragma unroll
+  for (int l = 0; l < K; ++l) {
+    // g of level l's output row: arrived with the u row of step kk - lR
+    // (stale during a level's warm-up: never stored then)
+    double g[4];
+    {
+      int gs = rs - l * R;
+      if (gs < 0) gs += p.stages;
+      const double* grow = sg + (size_t)gs * TG_::GROW + ls.uoff;
+      const double2 ga = *reinterpret_cast<const double2*>(grow);
+      const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
+      g[0] = ga.x; g[1] = ga.y; g[2] = gb.x; g[3] = gb.y;
+    }
+    const int G = ls.row_base + kk - (l + 1) * R;           // global row of the output
+    const bool rowin = (unsigned)G < (unsigned)p.rows;
     double o[4], dd[4];
-    level_row<STENCIL, K, FAST>(ws, ls, 0, ph + 1, sg + (size_t)cs * TG_::GROW + ls.uoff,
-                                (unsigned)G < (unsigned)p.rows, o, dd);
-    const bool active = kk >= 2 * R;
-    if (REDUCE && active && (unsigned)(G - ls.ja) < (unsigned)(ls.jb - ls.ja)) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double uw[P], x1[P], x2[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {                      // logical row q -> ring slot
+        const int sl = (ph + 1 + q) % P;
+        uw[q] = ws.u[l][sl][j];
+        x1[q] = ws.h1[l][sl][j];
+        x2[q] = ws.h2[l][sl][j];
+      }
+      const double J = Point<STENCIL>::jacobi_target(uw, x1, x2, g[j]);
+      dd[j] = __dsub_rn(J, uw[R]);
+      o[j] = (FAST || (rowin && ls.in[j])) ? __fma_rn(ws.wl[l], dd[j], uw[R]) : uw[R];
+    }
+    const bool active = kk >= 2 * (l + 1) * R;
+    if (REDUCE && l == 0 && active && (unsigned)(G - ls.ja) < (unsigned)(ls.jb - ls.ja)) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (ls.own[j]) { acc_s = __fma_rn(dd[j], dd[j], acc_s); acc_m = nan_max(acc_m, fabs(dd[j])); }
     }
-    if (K > 1) {
-      hand_over<R, K>(ws, 1, ph, o);
+    if (l + 1 < K) {
+      // neighbours of this lane's columns at level l: adjacent lanes (the two
+      // warp-edge lanes get their own values: garbage inside the lost halo)
+      const double l1 = __shfl_up_sync(0xffffffffu, o[3], 1);
+      const double r1 = __shfl_down_sync(0xffffffffu, o[0], 1);
+      double l2 = 0.0, r2 = 0.0;
+      if (R == 2) {
+        l2 = __shfl_up_sync(0xffffffffu, o[2], 1);
+        r2 = __shfl_down_sync(0xffffffffu, o[1], 1);
+      }
+      push_row<R, K>(ws, l + 1, ph, o, l2, l1, r1, r2);
     } else if (active) {
-      if (STORE) store_row<R, K, FAST>(ls, ls.outp, lane, o);
+      if (STORE) {
+        // FAST: every column is interior, ownership depends on the lane only
+        // (E even: both columns of a pair are owned or neither)
+        const bool own01 = FAST ? (4 * lane >= E && 4 * lane + 2 <= WG::WSPAN - E)
+                                : (ls.own[0] && ls.own[1]);
+        const bool own23 = FAST ? (4 * lane + 2 >= E && 4 * lane + 4 <= WG::WSPAN - E)
+                                : (ls.own[2] && ls.own[3]);
+        if (own01) *reinterpret_cast<double2*>(ls.outp) = make_double2(o[0], o[1]);
+        else if (!FAST) {
+          if (ls.own[0]) ls.outp[0] = o[0];
+          if (ls.own[1]) ls.outp[1] = o[1];
+        }
+        if (own23) *reinterpret_cast<double2*>(ls.outp + 2) = make_double2(o[2], o[3]);
+        else if (!FAST) {
+          if (ls.own[2]) ls.outp[2] = o[2];
+          if (ls.own[3]) ls.outp[3] = o[3];
+        }
+      }
       ls.outp += p.ld;
     }
   }
   // ---- release the slot whose last reader (level K-1's g) was this step
-  const int hold = (K - 1) * (R + 1);
-  if (kk >= hold) {
-    int rel = cs - hold;
-    while (rel < 0) rel += p.stages;
+  if (kk >= (K - 1) * R) {
+    int rel = rs - (K - 1) * R;
+    if (rel < 0) rel += p.stages;
     fence_proxy_async_smem();   // my reads of the slot before its TMA refill
     __syncwarp();
     if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * rel);
   }
-  if (++ls.cslot == p.stages) ls.cslot = 0;
 }
 
 template <int STENCIL, int NW, int K, bool REDUCE, bool STORE, bool FAST>
@@ -257,20 +228,16 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws
     }
     return;
   }
-  ls.cslot = ws.stage;
-  const int nsteps = nin + K - 1;                   // K-1 drain steps (level skew)
   int k0 = 0;
-  for (; k0 + P <= nsteps; k0 += P) {               // full periods: no guards
+  for (; k0 + P <= nin; k0 += P) {                  // full periods: no guards
 #pragma unroll
     for (int ph = 0; ph < P; ++ph)
-      warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, nin, lane,
-                                                     acc_s, acc_m);
+      warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s, acc_m);
   }
 #pragma unroll
   for (int ph = 0; ph < P - 1; ++ph)                 // tail
-    if (k0 + ph < nsteps)
-      warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, nin, lane,
-                                                     acc_s, acc_m);
+    if (k0 + ph < nin)
+      warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s, acc_m);
   // the last R(K-1) slots of the segment were still held: release them
   if (K > 1) {
     fence_proxy_async_smem();
