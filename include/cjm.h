@@ -105,6 +105,10 @@ typedef struct {
     int ctas_per_sm;       /* resident CTAs per SM of the persistent sweep grid */
     int stages;            /* depth of the TMA row ring */
     int graph_chunk;       /* sweeps captured per CUDA graph */
+    int resident;          /* hot sweeps of grids that fit in the SMs' shared memory run
+                              as ONE cooperative launch per cycle with the grid resident
+                              in shared memory: 0 = auto (default), 1 = required,
+                              -1 = never.  Single GPU only. */
     int band_split;        /* 1: run every K=1 hot sweep as boundary-band launches +
                               interior launch (the multi-GPU overlap schedule) even
                               without NCCL; for tests */
@@ -125,7 +129,8 @@ typedef struct {
     long long sweeps_timed;/* number of sweeps inside sweep_s */
     long long kernel_launches; /* kernels of this library launched by the call */
     long long hot_launches;    /* sweep-kernel launches inside sweep_s */
-    int temporal_k;            /* sweeps per hot launch */
+    int temporal_k;            /* sweeps per hot launch (streaming kernels) */
+    int resident;              /* 1: hot sweeps ran in the shared-memory-resident kernel */
     double h2d_bytes, d2h_bytes;  /* host<->device bytes moved by the call */
     double real_error;     /* cjm_solve_ref: max |u - u_ref| of the returned iterate */
 } cjm_report;

@@ -49,7 +49,7 @@ class Options(C.Structure):
                 ("temporal_k", C.c_int), ("variant", C.c_int),
                 ("tile_w", C.c_int),
                 ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int),
-                ("band_split", C.c_int)]
+                ("resident", C.c_int), ("band_split", C.c_int)]
 
 
 class HaloMsg(C.Structure):
@@ -64,7 +64,7 @@ class Report(C.Structure):
                 ("r_l2", C.c_double), ("r_linf", C.c_double),
                 ("plan_s", C.c_double), ("solve_s", C.c_double), ("sweep_s", C.c_double),
                 ("sweeps_timed", C.c_longlong), ("kernel_launches", C.c_longlong),
-                ("hot_launches", C.c_longlong), ("temporal_k", C.c_int),
+                ("hot_launches", C.c_longlong), ("temporal_k", C.c_int), ("resident", C.c_int),
                 ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("real_error", C.c_double)]
 
     def as_dict(self) -> dict:

@@ -27,6 +27,7 @@
 #include "internal.h"
 #include "sweep.cuh"
 #include "sweep_v4.cuh"
+#include "resident.cuh"
 
 namespace {
 
@@ -190,6 +191,12 @@ struct cjm_plan_s {
   int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
   int variant = 4;   // 3: shared-line levels (sweep.cuh), 4: warp-tiled (sweep_v4.cuh)
   int band_split = 0;  // split hot sweeps into boundary / interior bands even without NCCL
+  // resident (whole grid in shared memory) hot path
+  int resident = 0, res_ctas = 0, res_rows = 0;
+  size_t res_smem = 0;
+  double* res_halo = nullptr;
+  unsigned int* res_flags = nullptr;
+  size_t res_halo_bytes = 0;
   cudaStream_t cap_stream = nullptr;
   cudaStream_t comm_stream = nullptr;               // multi-GPU halo exchange
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -354,7 +361,51 @@ cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out,
 
 // Run `count` hot sweeps: blocks of K fused sweeps from CUDA graphs, the
 // remainder (< K) as single-sweep launches.  Returns the hot launch count.
+using ResidentFn = void (*)(const cjm::ResidentParams);
+
+ResidentFn pick_resident(int stencil) {
+  switch (stencil) {
+    case 5: return cjm::cjm_resident_kernel<5>;
+    case 9: return cjm::cjm_resident_kernel<9>;
+    default: return cjm::cjm_resident_kernel<17>;
+  }
+}
+
+// `count` sweeps in ONE cooperative launch with the grid resident in shared
+// memory (resident.cuh); reads buffer host_cur, writes host_cur ^ 1.
+cjm_status run_resident(cjm_plan_s* pl, long long count, cudaStream_t st) {
+  cjm::ResidentParams rp;
+  rp.buf[0] = pl->buf[0];
+  rp.buf[1] = pl->buf[1];
+  rp.g = pl->G;
+  rp.w = pl->w_dev;
+  rp.state = pl->state;
+  rp.halo = pl->res_halo;
+  rp.flags = pl->res_flags;
+  rp.P = pl->P;
+  rp.ld = pl->ld;
+  rp.nx = pl->nx;
+  rp.rows = pl->ny_local;
+  rp.count = (int)count;
+  rp.rows_per_cta = pl->res_rows;
+  CUDA_TRY(cudaMemsetAsync(pl->res_flags, 0, (size_t)pl->res_ctas * sizeof(unsigned int), st));
+  void* args[] = {&rp};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pick_resident(pl->stencil), dim3(pl->res_ctas),
+                                       dim3(512), args, pl->res_smem, st));
+  pl->launches += 1;
+  pl->host_cur ^= 1;
+  return CJM_OK;
+}
+
+// Run `count` hot sweeps: blocks of K fused sweeps from CUDA graphs, the
+// remainder (< K) as single-sweep launches -- or, for grids resident in
+// shared memory, one cooperative launch.  Counts hot launches.
 cjm_status run_hot(cjm_plan_s* pl, long long count, cudaStream_t st, long long* hot_launches) {
+  if (pl->resident && count >= 8 && count < (1LL << 31)) {
+    STATUS_TRY(run_resident(pl, count, st));
+    *hot_launches += 1;
+    return CJM_OK;
+  }
   const int K = pl->K;
   long long blocks = count / K;
   const long long rem = count % K;
@@ -471,6 +522,7 @@ void fill_static(const cjm_plan_s* pl, cjm_report* r) {
   r->kappa_max = pl->sched.kmax;
   r->plan_s = pl->plan_s;
   r->temporal_k = pl->K;
+  r->resident = pl->resident;
 }
 
 // The whole solve (rows a5-a10); `kin` / `kout` select device or host user buffers.
@@ -681,6 +733,8 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   cjm::pool_free(p->device, p->g_elems * sizeof(double), p->G);
   cjm::pool_free(p->device, (size_t)p->P * sizeof(double), p->w_dev);
   cjm::pool_free(p->device, p->small_bytes, p->small_block);
+  if (p->res_halo) cjm::pool_free(p->device, p->res_halo_bytes, p->res_halo);
+  if (p->res_flags) cjm::pool_free(p->device, (size_t)p->res_ctas * sizeof(unsigned int), p->res_flags);
   cjm::pool_free_host(2 * sizeof(double), p->result_host);
   if (p->comm) ncclCommDestroy(p->comm);
   tt.mark("free");
@@ -829,6 +883,39 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   }
   pl->nctas = nsm * std::min(occ_min, pl->ctas_per_sm);
 
+  // ---- resident (shared-memory) hot path: single GPU, whole grid fits in the
+  // SMs' shared memory with at least 16 rows per CTA
+  if (pl->world == 1 && opt.resident >= 0) {
+    const int ldS = nx + 2 * R;
+    auto smem_for = [&](int rows) {
+      return ((size_t)2 * (rows + 2 * R) * ldS + (size_t)rows * nx) * sizeof(double);
+    };
+    // at least 16 rows per CTA for small grids (fewer handshakes), else the
+    // minimum slab height that spreads the grid over all SMs
+    const int rows_min = (nyl + nsm - 1) / nsm;
+    int rows = std::max(rows_min, std::min(16, nyl));
+    if (smem_for(rows) + 1024 > (size_t)smem_optin) rows = rows_min;
+    const int ctas = (nyl + rows - 1) / rows;
+    const size_t smem = smem_for(rows);
+    int occ_r = 0;
+    if (smem + 1024 <= (size_t)smem_optin) {
+      ResidentFn rf = pick_resident(stencil);
+      PLAN_CUDA(cudaFuncSetAttribute((const void*)rf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, (const void*)rf, 512, smem));
+    }
+    if (occ_r >= 1 && ctas <= nsm * occ_r) {
+      pl->resident = 1;
+      pl->res_rows = rows;
+      pl->res_ctas = ctas;
+      pl->res_smem = smem;
+      pl->res_halo_bytes = (size_t)ctas * 2 * 2 * R * ldS * sizeof(double);
+    } else if (opt.resident == 1) {
+      set_error("cjm_plan", "resident=1 but the grid does not fit in shared memory");
+      return fail(CJM_ERR_INVALID_ARG);
+    }
+  }
+
   tt.mark("schedule+config");
   // ---- buffers: (ny_local + 2R) rows of pitch ld; interior column 0 at PADL
   pl->ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
@@ -849,6 +936,10 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
                     sizeof(unsigned long long);
   PLAN_CUDA(cjm::pool_alloc(dev, pl->small_bytes, &pl->small_block));
   pl->partials = static_cast<double*>(pl->small_block);
+  if (pl->resident) {
+    PLAN_CUDA(cjm::pool_alloc(dev, pl->res_halo_bytes, (void**)&pl->res_halo));
+    PLAN_CUDA(cjm::pool_alloc(dev, (size_t)pl->res_ctas * sizeof(unsigned int), (void**)&pl->res_flags));
+  }
   pl->result = pl->partials + (size_t)pl->nctas * 2;
   pl->state = reinterpret_cast<cjm::SweepState*>(pl->result + 2);
   pl->err_bits = reinterpret_cast<unsigned long long*>(pl->state + 1);

@@ -1,0 +1,153 @@
+// sm_100a fp64 CJM sweeps with the whole grid resident in shared memory
+// (the persistent small-grid kernel, part of NEXT-1).
+//
+// When u, u' and g of the whole (single-GPU) grid fit in the aggregate shared
+// memory of the SMs (148 x 227 KB = 33 MB: up to ~1100^2 for the 9-point),
+// one cooperative launch runs `count` consecutive sweeps without touching HBM
+// in between: every CTA owns a slab of rows, loads its rows of u (with r halo
+// rows and the ghost columns) and of g once, sweeps them in shared memory
+// (double-buffered), and after each sweep exchanges its r boundary rows with
+// the two neighbouring CTAs through a small global halo area and per-CTA
+// release / acquire flags (no grid-wide barrier).  At the end it writes its
+// rows to the output buffer.  Per sweep that costs one neighbour handshake
+// (~1 us through L2) instead of a kernel launch and a full pass over L2/HBM.
+//
+// Same per-point association (DESIGN R6), same weights w[(n+k) mod P] and the
+// same device-side state protocol as the streaming kernels (reads buffer cur,
+// writes cur^1, advances n by count), so results are bitwise identical.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "sweep.cuh"
+
+namespace cjm {
+
+struct ResidentParams {
+  double* buf[2];
+  const double* g;
+  const double* w;
+  SweepState* state;
+  double* halo;                 // [grid][2 parities][2 sides][R rows][ldh]
+  unsigned int* flags;          // [grid], zeroed before the launch
+  long long P, ld;
+  int nx, rows;                 // interior columns / rows
+  int count;                    // sweeps of this launch
+  int rows_per_cta;             // slab height (the last CTA may have fewer)
+};
+
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int STENCIL>
+__global__ void __launch_bounds__(512, 1) cjm_resident_kernel(const ResidentParams p) {
+  constexpr int R = Point<STENCIL>::R;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int ldS = p.nx + 2 * R;                 // shared row: ghost columns included
+  const int r0 = blockIdx.x * p.rows_per_cta;   // first interior row of my slab
+  const int nr = min(p.rows_per_cta, p.rows - r0);
+  const int srows = nr + 2 * R;                 // + halo / ghost rows
+  double* sbuf[2];
+  sbuf[0] = reinterpret_cast<double*>(smem_raw);
+  sbuf[1] = sbuf[0] + (size_t)srows * ldS;
+  double* sg = sbuf[1] + (size_t)srows * ldS;   // nr x nx
+
+  const unsigned long long n0 = __ldcg(&p.state->n);
+  const unsigned int cur = __ldcg(&p.state->cur);
+  const double* src = (cur & 1u) ? p.buf[1] : p.buf[0];
+  double* dst = (cur & 1u) ? p.buf[0] : p.buf[1];
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  // ---- load my rows (and halo / ghost rows, ghost columns) of u into both
+  // shared buffers, and my rows of g
+  for (int e = tid; e < srows * ldS; e += nt) {
+    const int q = e / ldS, c = e - q * ldS;    // local row q <-> interior row r0 - R + q
+    const double v = src[(long long)(r0 + q) * p.ld + (PADL - R) + c];
+    sbuf[0][e] = v;
+    sbuf[1][e] = v;
+  }
+  for (int e = tid; e < nr * p.nx; e += nt) {
+    const int q = e / p.nx, c = e - q * p.nx;
+    sg[e] = p.g[(long long)(r0 + q) * p.ld + PADL + c];
+  }
+  __syncthreads();
+
+  const int ldh = ldS;
+  double* my_halo = p.halo + (size_t)blockIdx.x * 2 * 2 * R * ldh;
+  const bool has_up = blockIdx.x > 0, has_dn = blockIdx.x + 1 < gridDim.x;
+  int sc = 0;
+  for (int k = 0; k < p.count; ++k) {
+    const double w = __ldg(p.w + (long long)((n0 + k) % (unsigned long long)p.P));
+    const double* a = sbuf[sc];
+    double* b = sbuf[sc ^ 1];
+    // ---- one sweep of my slab, shared -> shared
+    for (int e = tid; e < nr * p.nx; e += nt) {
+      const int q = e / p.nx, i = e - q * p.nx;
+      const int c = (q + R) * ldS + (i + R);   // shared index of node (i, r0+q)
+      double uc[2 * R + 1], h1[2 * R + 1], h2[2 * R + 1];
+#pragma unroll
+      for (int t = 0; t < 2 * R + 1; ++t) {
+        const int cc = c + (t - R) * ldS;
+        uc[t] = a[cc];
+        h1[t] = __dadd_rn(a[cc - 1], a[cc + 1]);
+        h2[t] = (R == 2) ? __dadd_rn(a[cc - 2], a[cc + 2]) : 0.0;
+      }
+      const double J = Point<STENCIL>::jacobi_target(uc, h1, h2, sg[e]);
+      b[c] = __fma_rn(w, __dsub_rn(J, uc[R]), uc[R]);
+    }
+    __syncthreads();
+    if (k + 1 == p.count) { sc ^= 1; break; }
+    // ---- publish my boundary rows, then take the neighbours'
+    double* hb = my_halo + (size_t)(k & 1) * 2 * R * ldh;
+    for (int e = tid; e < R * p.nx; e += nt) {
+      const int q = e / p.nx, i = e - q * p.nx;
+      hb[(size_t)q * ldh + i] = b[(q + R) * ldS + i + R];                     // first rows
+      hb[(size_t)(R + q) * ldh + i] = b[(nr + q) * ldS + i + R];              // last rows
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(p.flags + blockIdx.x, (unsigned)k + 1u);
+      if (has_up) while (ld_acquire_u32(p.flags + blockIdx.x - 1) < (unsigned)k + 1u) {}
+      if (has_dn) while (ld_acquire_u32(p.flags + blockIdx.x + 1) < (unsigned)k + 1u) {}
+    }
+    __syncthreads();
+    if (has_up) {
+      const double* nb = p.halo + ((size_t)(blockIdx.x - 1) * 2 + (k & 1)) * 2 * R * ldh;
+      for (int e = tid; e < R * p.nx; e += nt) {
+        const int q = e / p.nx, i = e - q * p.nx;
+        b[q * ldS + i + R] = __ldcg(nb + (size_t)(R + q) * ldh + i);        // its last rows
+      }
+    }
+    if (has_dn) {
+      const double* nb = p.halo + ((size_t)(blockIdx.x + 1) * 2 + (k & 1)) * 2 * R * ldh;
+      for (int e = tid; e < R * p.nx; e += nt) {
+        const int q = e / p.nx, i = e - q * p.nx;
+        b[(nr + R + q) * ldS + i + R] = __ldcg(nb + (size_t)q * ldh + i);   // its first rows
+      }
+    }
+    __syncthreads();
+    sc ^= 1;
+  }
+  // ---- write my rows of the result
+  const double* fin = sbuf[sc];
+  for (int e = tid; e < nr * p.nx; e += nt) {
+    const int q = e / p.nx, i = e - q * p.nx;
+    dst[(long long)(r0 + q + R) * p.ld + PADL + i] = fin[(q + R) * ldS + i + R];
+  }
+  // ---- advance the device-side state (the whole grid is one launch: use
+  // the grid group to let exactly one thread do it after everyone finished)
+  cooperative_groups::this_grid().sync();
+  if (blockIdx.x == 0 && tid == 0) {
+    p.state->n = n0 + (unsigned long long)p.count;
+    p.state->cur = cur ^ 1u;
+  }
+}
+
+}  // namespace cjm

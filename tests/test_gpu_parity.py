@@ -86,7 +86,7 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=3)
     with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=4, temporal_k=temporal_k,
-                  variant=variant) as plan:
+                  variant=variant, resident=-1) as plan:
         w = plan.info()["weights"]
         ud = dev(u0)
         plan.sweeps(dev(b), ud, 5, count)
@@ -109,7 +109,7 @@ def test_launch_configuration_does_not_change_result(cfg):
     u0, b, h = inputs.test_problem(nx, ny, 1, init="random", seed=5)
     outs = []
     for kw in (dict(), cfg):
-        with cjm.Plan(9, nx, ny, h, 1e-8, **kw) as plan:
+        with cjm.Plan(9, nx, ny, h, 1e-8, resident=-1, **kw) as plan:
             ud = dev(u0)
             plan.sweeps(dev(b), ud, 0, 40)
             outs.append(host(ud))
@@ -132,14 +132,17 @@ def test_residual_matches_oracle(stencil):  # noqa: D103
 # ------------------------------------------------------------ full solves
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("n,init", [(64, "zero"), (64, "random"), (200, "zero"), (129, "random")])
-@pytest.mark.parametrize("temporal_k,variant", [(1, 4), (2, 4), (2, 3), (4, 3), (3, 0)])
-def test_solve_matches_oracle(stencil, n, init, temporal_k, variant):
+@pytest.mark.parametrize("temporal_k,variant,resident", [(1, 4, -1), (2, 4, -1), (2, 3, -1), (4, 3, -1),
+                                                          (3, 0, -1), (0, 0, 1)])
+def test_solve_matches_oracle(stencil, n, init, temporal_k, variant, resident):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(n, n, r, init=init)
     uo, ro = oracle.solve(stencil, h, 1e-8, b, u0)
     if stencil == 17 and variant == 4 and temporal_k > 1:
         variant = 0
-    with cjm.Plan(stencil, n, n, h, 1e-8, temporal_k=temporal_k, variant=variant) as plan:
+    with cjm.Plan(stencil, n, n, h, 1e-8, temporal_k=temporal_k, variant=variant,
+                  resident=resident) as plan:
+        assert plan.info()["resident"] == (1 if resident == 1 else 0)
         ud = dev(u0)
         rep = plan.solve(dev(b), ud)
     assert rep["status"] == "CJM_OK" and ro["status"] == "OK"
@@ -238,8 +241,8 @@ def _digest_cases():
 
 
 @pytest.mark.parametrize("name", _digest_cases())
-@pytest.mark.parametrize("temporal_k", (1, 2))
-def test_solve_matches_stored_oracle_digest(name, temporal_k):  # noqa: D103
+@pytest.mark.parametrize("temporal_k,resident", [(1, -1), (2, -1), (0, 0)])
+def test_solve_matches_stored_oracle_digest(name, temporal_k, resident):  # noqa: D103
     """Full solves at BASELINE sizes vs the oracle's stored result
     (tests/make_oracle_digests.py): same iterations, sampled nodes within
     1e-10 max|u| and bitwise, and the SHA-256 of the whole interior."""
@@ -252,7 +255,7 @@ def test_solve_matches_stored_oracle_digest(name, temporal_k):  # noqa: D103
     r = oracle.reach(st)
     u0, b, h2 = inputs.test_problem(nx, ny, r, init=rec["init"])
     assert h2 == h
-    with cjm.Plan(st, nx, ny, h, tol, temporal_k=temporal_k) as plan:
+    with cjm.Plan(st, nx, ny, h, tol, temporal_k=temporal_k, resident=resident) as plan:
         ud = dev(u0)
         rep = plan.solve(dev(b), ud)
     assert rep["status"] == "CJM_OK"
@@ -303,3 +306,27 @@ def test_real_error_below_discretisation_error_does_not_converge():
         rep = plan.solve_ref(dev(b), dev(u0), dev(ex), 1e-9, ok=(3, 5))
     assert rep["status"] in ("CJM_ERR_STAGNATED", "CJM_ERR_NOT_CONVERGED")
     assert rep["real_error"] > 1e-9
+
+
+# ------------------------------------------------------------ shared-memory-resident hot path
+@pytest.mark.parametrize("stencil", (5, 9, 17))
+@pytest.mark.parametrize("nx,ny,count", [(64, 64, 324), (300, 257, 37), (130, 1000, 20), (1024, 1024, 16),
+                                         (9, 700, 13), (4, 4, 9), (500, 17, 8)])
+def test_resident_segment_bitwise(stencil, nx, ny, count):
+    """The cooperative shared-memory kernel (one launch for the whole
+    segment, neighbour handshakes between CTA slabs) vs the oracle."""
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=13)
+    try:
+        plan = cjm.Plan(stencil, nx, ny, h, 1e-8, resident=1)
+    except cjm.CJMError as e:
+        assert e.name == "CJM_ERR_INVALID_ARG" and nx * ny >= 1024 * 1024
+        pytest.skip("grid does not fit in shared memory")
+    with plan:
+        w = plan.info()["weights"]
+        ud = dev(u0)
+        rep = plan.sweeps(dev(b), ud, 3, count)
+        assert rep["resident"] == 1 and rep["hot_launches"] == 1
+        g = oracle.rhs_to_g(stencil, h, b)
+        want = oracle.sweeps(stencil, u0, g, w, 3, count)
+        assert_field_parity(host(ud), want, r)

@@ -28,7 +28,22 @@ def test_ring_reuse_is_race_free(variant, K, stages):
     ref = oracle.sweeps(5, u0, oracle.rhs_to_g(5, h, b), s["w"], 0, cnt)
     bd = torch.from_numpy(b).cuda()
     bad = 0
-    with cjm.Plan(5, n, n, h, 1e-8, temporal_k=K, variant=variant, stages=stages) as plan:
+    with cjm.Plan(5, n, n, h, 1e-8, temporal_k=K, variant=variant, stages=stages, resident=-1) as plan:
+        for _ in range(trials):
+            ud = torch.from_numpy(u0.copy()).cuda()
+            plan.sweeps(bd, ud, 0, cnt)
+            bad += not np.array_equal(ud.cpu().numpy(), ref)
+    assert bad == 0, f"{bad} of {trials} runs differ from the oracle"
+
+
+def test_resident_handshakes_are_race_free():
+    n, cnt, trials = 1024, 64, 30
+    u0, b, h = inputs.test_problem(n, n, 1, init="random")
+    s = oracle.schedule(9, n, n, 1e-8)
+    ref = oracle.sweeps(9, u0, oracle.rhs_to_g(9, h, b), s["w"], 0, cnt)
+    bd = torch.from_numpy(b).cuda()
+    bad = 0
+    with cjm.Plan(9, n, n, h, 1e-8, resident=1) as plan:
         for _ in range(trials):
             ud = torch.from_numpy(u0.copy()).cuda()
             plan.sweeps(bd, ud, 0, cnt)
