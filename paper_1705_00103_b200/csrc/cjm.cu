@@ -904,7 +904,11 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
                                      (int)smem));
       PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, (const void*)rf, 512, smem));
     }
-    if (occ_r >= 1 && ctas <= nsm * occ_r) {
+    // auto mode only where the neighbour handshakes do not dominate: at most
+    // 4 CTA slabs (the 64^2 config: 2.9 vs 3.8 us per sweep; from 128^2 on
+    // the streaming kernels win, profiles/r01_resident_vs_stream.jsonl)
+    const bool wanted = opt.resident == 1 || ctas <= 4;
+    if (occ_r >= 1 && ctas <= nsm * occ_r && wanted) {
       pl->resident = 1;
       pl->res_rows = rows;
       pl->res_ctas = ctas;
