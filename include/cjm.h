@@ -35,7 +35,11 @@
  *    [y0, y0 + ny_local) of the global interior rows (cjm_plan_info); u and
  *    rhs are then the LOCAL slab (rows_u = ny_local + 2r, rhs ny_local rows).
  *    Ghost rows that border another rank are filled by the library (halo
- *    exchange); only ranks 0 and world_size-1 need real top / bottom data.
+ *    exchange of K r rows after every K-fused launch); only
+ *    ranks 0 and world_size-1 need real top / bottom data.  external_halo
+ *    plans with temporal_k = K > 1 instead take u with H = K r ghost rows and
+ *    rhs with H extra rows above and below (the neighbours' rows, refreshed
+ *    by the caller): cjm_report.ghost_rows / rhs_ghost_rows say how many.
  *  - Every call returns a cjm_status; no exception crosses the ABI.  On
  *    CJM_ERR_CUDA / CJM_ERR_NCCL, cjm_last_error() gives the message.
  *  - Thread compatibility: a plan may be used by one host thread at a time.
@@ -131,6 +135,8 @@ typedef struct {
     long long hot_launches;    /* sweep-kernel launches inside sweep_s */
     int temporal_k;            /* sweeps per hot launch (streaming kernels) */
     int resident;              /* 1: hot sweeps ran in the shared-memory-resident kernel */
+    int ghost_rows;            /* ghost rows above / below the slab in the caller's u */
+    int rhs_ghost_rows;        /* extra rows above / below the slab in the caller's rhs */
     double h2d_bytes, d2h_bytes;  /* host<->device bytes moved by the call */
     double real_error;     /* cjm_solve_ref: max |u - u_ref| of the returned iterate */
 } cjm_report;
@@ -243,12 +249,13 @@ typedef struct {
 } cjm_halo_msg;
 
 /* Host-only halo plan of rank `rank` of `world_size` for a global grid of
- * ny interior rows and stencil reach r: one message per neighbour slab
+ * ny interior rows and halo depth r (the stencil reach, or K r for K-fused
+ * launches; 1..16): one message per neighbour slab
  * (0, 1 or 2).  My first r interior rows go to the neighbour above (rank-1),
  * into its last ghost rows; my last r interior rows go to the neighbour below
  * (rank+1), into its first ghost rows.  msgs must hold 2 entries.
  * Errors: INVALID_ARG (sizes, a slab thinner than 2r+1 rows when
- * world_size > 1, r not 1 or 2). */
+ * world_size > 1, r outside 1..16). */
 cjm_status cjm_halo_plan(int ny, int r, int world_size, int rank, cjm_halo_msg *msgs,
                          int *nmsgs);
 

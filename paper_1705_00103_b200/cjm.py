@@ -65,6 +65,7 @@ class Report(C.Structure):
                 ("plan_s", C.c_double), ("solve_s", C.c_double), ("sweep_s", C.c_double),
                 ("sweeps_timed", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("hot_launches", C.c_longlong), ("temporal_k", C.c_int), ("resident", C.c_int),
+                ("ghost_rows", C.c_int), ("rhs_ghost_rows", C.c_int),
                 ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("real_error", C.c_double)]
 
     def as_dict(self) -> dict:
@@ -208,6 +209,7 @@ class Plan:
         self.stencil, self.nx, self.ny, self.h, self.tol = stencil, nx, ny, h, tol
         info = self.info()
         self.reach, self.y0, self.ny_local = info["reach"], info["y0"], info["ny_local"]
+        self.ghost_rows, self.rhs_ghost_rows = info["ghost_rows"], info["rhs_ghost_rows"]
         self.P = info["cycle_len"]
 
     def info(self) -> dict:
@@ -220,12 +222,13 @@ class Plan:
         return d
 
     def _check_shapes(self, rhs, u):
-        r = self.reach
-        if tuple(u.shape) != (self.ny_local + 2 * r, self.nx + 2 * r):
+        r, gu, gr = self.reach, self.ghost_rows, self.rhs_ghost_rows
+        if tuple(u.shape) != (self.ny_local + 2 * gu, self.nx + 2 * r):
             raise ValueError(f"u: shape {tuple(u.shape)}, plan expects "
-                             f"{(self.ny_local + 2 * r, self.nx + 2 * r)}")
-        if tuple(rhs.shape) != (self.ny_local, self.nx):
-            raise ValueError(f"rhs: shape {tuple(rhs.shape)}, plan expects {(self.ny_local, self.nx)}")
+                             f"{(self.ny_local + 2 * gu, self.nx + 2 * r)}")
+        if tuple(rhs.shape) != (self.ny_local + 2 * gr, self.nx):
+            raise ValueError(f"rhs: shape {tuple(rhs.shape)}, plan expects "
+                             f"{(self.ny_local + 2 * gr, self.nx)}")
 
     def solve(self, rhs, u, stream=None, ok=(0,)) -> dict:
         """cjm_solve on device tensors; u is updated in place."""

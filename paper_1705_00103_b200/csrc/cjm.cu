@@ -167,6 +167,10 @@ __global__ void set_state_kernel(cjm::SweepState* st, unsigned long long n) {
 struct cjm_plan_s {
   // problem
   int stencil = 9, R = 1, nx = 0, ny = 0, y0 = 0, ny_local = 0;
+  // ghost rows: H stored above / below the slab in buf and G (r, or K r for
+  // multi-GPU deep halos); Hu of them in the user's u, Hr in the user's rhs;
+  // local rows [row_lo, row_hi) are interior rows of the global grid
+  int H = 1, Hu = 1, Hr = 0, row_lo = 0, row_hi = 0;
   double h = 0, tol = 0, gscale = 0;
   int method = CJM_METHOD_CHEBYSHEV, max_cycles = 8;
   cjm::Schedule sched;
@@ -258,6 +262,9 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int ro
   sp.ld = pl->ld;
   sp.nx = pl->nx;
   sp.rows = pl->ny_local;
+  sp.H = pl->H;
+  sp.row_lo = pl->row_lo;
+  sp.row_hi = pl->row_hi;
   sp.row0 = row0;
   sp.nrows = nrows;
   sp.stages = pl->stages;
@@ -282,7 +289,7 @@ cjm_status halo_exchange(cjm_plan_s* pl, double* b, cudaStream_t st) {
   if (pl->world == 1 || !pl->comm) return CJM_OK;   // external_halo: the caller moves them
   cjm_halo_msg msgs[2];
   int nm = 0;
-  STATUS_TRY(cjm_halo_plan(pl->ny, pl->R, pl->world, pl->rank, msgs, &nm));
+  STATUS_TRY(cjm_halo_plan(pl->ny, pl->H, pl->world, pl->rank, msgs, &nm));
   NCCL_TRY(ncclGroupStart());
   for (int k = 0; k < nm; ++k) {
     const size_t cnt = (size_t)msgs[k].rows * pl->ld;
@@ -304,16 +311,18 @@ cjm_status halo_exchange(cjm_plan_s* pl, double* b, cudaStream_t st) {
 // that advances n / cur.  Check sweeps (the reduction must cover every row of
 // one launch) are not split.
 cjm_status sweep_and_exchange(cjm_plan_s* pl, int mode, int K, cudaStream_t st) {
-  const int R = pl->R, nyl = pl->ny_local;
-  if (mode == MODE_HOT && (pl->comm || pl->band_split) && K == 1 && nyl > 4 * R) {
-    STATUS_TRY(launch_sweep(pl, mode, K, st, 0, R, 0));
-    STATUS_TRY(launch_sweep(pl, mode, K, st, nyl - R, R, 0));
+  const int Hh = pl->H, nyl = pl->ny_local;
+  if (mode == MODE_HOT && (pl->comm || pl->band_split) && nyl > 4 * Hh) {
+    // the neighbours need my first / last H rows (H = K r: the deep halo of a
+    // K-fused launch)
+    STATUS_TRY(launch_sweep(pl, mode, K, st, 0, Hh, 0));
+    STATUS_TRY(launch_sweep(pl, mode, K, st, nyl - Hh, Hh, 0));
     double* out = pl->buf[pl->host_cur ^ 1];    // the buffer this sweep writes
     CUDA_TRY(cudaEventRecord(pl->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(pl->comm_stream, pl->ev_fork, 0));
     STATUS_TRY(halo_exchange(pl, out, pl->comm_stream));
     CUDA_TRY(cudaEventRecord(pl->ev_join, pl->comm_stream));
-    STATUS_TRY(launch_sweep(pl, mode, K, st, R, nyl - 2 * R, 1));
+    STATUS_TRY(launch_sweep(pl, mode, K, st, Hh, nyl - 2 * Hh, 1));
     CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_join, 0));
     return CJM_OK;
   }
@@ -448,7 +457,7 @@ cjm_status real_error(cjm_plan_s* pl, int which, const double* ref, long long ld
   CUDA_TRY(cudaMemsetAsync(pl->err_bits, 0, sizeof(unsigned long long), st));
   const long long total = (long long)pl->nx * pl->ny_local;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
-  cjm::cjm_error_kernel<<<blocks, 256, 0, st>>>(pl->buf[which], pl->ld, pl->R, ref, ld_ref, pl->nx,
+  cjm::cjm_error_kernel<<<blocks, 256, 0, st>>>(pl->buf[which], pl->ld, pl->H, ref, ld_ref, pl->nx,
                                                 pl->ny_local, pl->err_bits);
   CUDA_TRY(cudaGetLastError());
   pl->launches += 1;
@@ -470,25 +479,32 @@ cjm_status set_state(cjm_plan_s* pl, unsigned long long n, cudaStream_t st) {
   return CJM_OK;
 }
 
-// Row a5: user layout -> internal buffers.  kind = H2D or D2D.
+// Row a5: user layout -> internal buffers.  kind = H2D or D2D.  The user's u
+// carries Hu ghost rows (r, or K r for external-halo deep halos) and r ghost
+// columns; rhs carries Hr extra rows (0, or H for external-halo deep halos).
 cjm_status stage_in(cjm_plan_s* pl, const double* rhs, long long ld_rhs, const double* u,
                     long long ld_u, bool both, cudaMemcpyKind kind, cudaStream_t st) {
   const int R = pl->R;
   const size_t upitch = (size_t)pl->ld * sizeof(double);
-  CUDA_TRY(cudaMemcpy2DAsync(pl->buf[0] + (cjm::PADL - R), upitch, u, (size_t)ld_u * sizeof(double),
-                             (size_t)(pl->nx + 2 * R) * sizeof(double), (size_t)(pl->ny_local + 2 * R),
-                             kind, st));
+  CUDA_TRY(cudaMemcpy2DAsync(pl->buf[0] + (long long)(pl->H - pl->Hu) * pl->ld + (cjm::PADL - R), upitch,
+                             u, (size_t)ld_u * sizeof(double),
+                             (size_t)(pl->nx + 2 * R) * sizeof(double),
+                             (size_t)(pl->ny_local + 2 * pl->Hu), kind, st));
   if (both)
     CUDA_TRY(cudaMemcpyAsync(pl->buf[1], pl->buf[0], pl->buf_elems * sizeof(double),
                              cudaMemcpyDeviceToDevice, st));
   if (rhs) {
-    CUDA_TRY(cudaMemcpy2DAsync(pl->G + cjm::PADL, upitch, rhs, (size_t)ld_rhs * sizeof(double),
-                               (size_t)pl->nx * sizeof(double), (size_t)pl->ny_local, kind, st));
-    const long long total = (long long)pl->nx * pl->ny_local;
+    double* g0 = pl->G + (long long)(pl->H - pl->Hr) * pl->ld;
+    const int grows = pl->ny_local + 2 * pl->Hr;
+    CUDA_TRY(cudaMemcpy2DAsync(g0 + cjm::PADL, upitch, rhs, (size_t)ld_rhs * sizeof(double),
+                               (size_t)pl->nx * sizeof(double), (size_t)grows, kind, st));
+    const long long total = (long long)pl->nx * grows;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-    cjm::cjm_scale_kernel<<<blocks, 256, 0, st>>>(pl->G, pl->ld, pl->nx, pl->ny_local, pl->gscale);
+    cjm::cjm_scale_kernel<<<blocks, 256, 0, st>>>(g0, pl->ld, pl->nx, grows, pl->gscale);
     CUDA_TRY(cudaGetLastError());
     pl->launches += 1;
+    // NCCL plans with deep halos: the neighbours' g rows (once per solve)
+    if (pl->comm && pl->H > pl->R) STATUS_TRY(halo_exchange(pl, pl->G, st));
   }
   return CJM_OK;
 }
@@ -496,8 +512,8 @@ cjm_status stage_in(cjm_plan_s* pl, const double* rhs, long long ld_rhs, const d
 cjm_status stage_out(cjm_plan_s* pl, int which, double* u, long long ld_u, cudaMemcpyKind kind,
                      cudaStream_t st) {
   const int R = pl->R;
-  CUDA_TRY(cudaMemcpy2DAsync(u + (long long)R * ld_u + R, (size_t)ld_u * sizeof(double),
-                             pl->buf[which] + (long long)R * pl->ld + cjm::PADL,
+  CUDA_TRY(cudaMemcpy2DAsync(u + (long long)pl->Hu * ld_u + R, (size_t)ld_u * sizeof(double),
+                             pl->buf[which] + (long long)pl->H * pl->ld + cjm::PADL,
                              (size_t)pl->ld * sizeof(double), (size_t)pl->nx * sizeof(double),
                              (size_t)pl->ny_local, kind, st));
   return CJM_OK;
@@ -523,6 +539,8 @@ void fill_static(const cjm_plan_s* pl, cjm_report* r) {
   r->plan_s = pl->plan_s;
   r->temporal_k = pl->K;
   r->resident = pl->resident;
+  r->ghost_rows = pl->Hu;
+  r->rhs_ghost_rows = pl->Hr;
 }
 
 // The whole solve (rows a5-a10); `kin` / `kout` select device or host user buffers.
@@ -551,8 +569,8 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
   CUDA_TRY(cudaEventRecord(pl->ev[0], st));
   STATUS_TRY(stage_in(pl, rhs, ld_rhs, u, ld_u, true, kin, st));
   if (kin == cudaMemcpyHostToDevice) {
-    rep.h2d_bytes = (double)(pl->ny_local + 2 * pl->R) * (pl->nx + 2 * pl->R) * 8.0 +
-                    (double)pl->ny_local * pl->nx * 8.0;
+    rep.h2d_bytes = (double)(pl->ny_local + 2 * pl->Hu) * (pl->nx + 2 * pl->R) * 8.0 +
+                    (double)(pl->ny_local + 2 * pl->Hr) * pl->nx * 8.0;
   }
   STATUS_TRY(set_state(pl, 0ull, st));
   STATUS_TRY(halo_exchange(pl, pl->buf[0], st));
@@ -680,7 +698,7 @@ cjm_status cjm_slab(int ny, int world_size, int rank, int* y0, int* ny_local) {
 cjm_status cjm_halo_plan(int ny, int r, int world_size, int rank, cjm_halo_msg* msgs,
                          int* nmsgs) {
   int y0 = 0, nyl = 0;
-  if (!msgs || !nmsgs || (r != 1 && r != 2) || cjm_slab(ny, world_size, rank, &y0, &nyl) != CJM_OK ||
+  if (!msgs || !nmsgs || r < 1 || r > 16 || cjm_slab(ny, world_size, rank, &y0, &nyl) != CJM_OK ||
       (world_size > 1 && nyl < 2 * r + 1)) {
     set_error("cjm_halo_plan", "invalid argument");
     return CJM_ERR_INVALID_ARG;
@@ -837,7 +855,9 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   pl->variant = opt.variant ? opt.variant : (wide ? 3 : 4);
   pl->band_split = opt.band_split;
   pl->K = opt.temporal_k > 0 ? opt.temporal_k : (wide ? 1 : 2);
-  if (pl->world > 1) pl->K = 1;   // deep halos for K > 1 across ranks: not implemented
+  // multi-GPU: K-fused launches need H = K r deep halos, exchanged after every
+  // launch; the slab must stay thicker than 2H + 1 rows (else fall back to K=1)
+  if (pl->world > 1 && nyl < 2 * pl->K * R + 1) pl->K = 1;
   if (stencil == 17 && pl->K > 1) {
     if (opt.variant == 4) {
       set_error("cjm_plan", "variant 4 supports the 17-point stencil with temporal_k = 1 only");
@@ -923,8 +943,13 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   tt.mark("schedule+config");
   // ---- buffers: (ny_local + 2R) rows of pitch ld; interior column 0 at PADL
   pl->ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
-  pl->buf_elems = (size_t)(nyl + 2 * R) * pl->ld;
-  pl->g_elems = (size_t)nyl * pl->ld;
+  pl->H = pl->world > 1 ? pl->K * R : R;
+  pl->Hu = (pl->world > 1 && opt.external_halo) ? pl->H : R;
+  pl->Hr = (pl->world > 1 && opt.external_halo) ? pl->H : 0;
+  pl->row_lo = std::max(-pl->H, -pl->y0);
+  pl->row_hi = std::min(nyl + pl->H, ny - pl->y0);
+  pl->buf_elems = (size_t)(nyl + 2 * pl->H) * pl->ld;
+  pl->g_elems = (size_t)(nyl + 2 * pl->H) * pl->ld;
   PLAN_CUDA(cjm::pool_alloc(dev, pl->buf_elems * sizeof(double), (void**)&pl->buf[0]));
   PLAN_CUDA(cjm::pool_alloc(dev, pl->buf_elems * sizeof(double), (void**)&pl->buf[1]));
   PLAN_CUDA(cjm::pool_alloc(dev, pl->g_elems * sizeof(double), (void**)&pl->G));

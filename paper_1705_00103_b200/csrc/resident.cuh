@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(512, 1) cjm_resident_kernel(const ResidentPara
   }
   for (int e = tid; e < nr * p.nx; e += nt) {
     const int q = e / p.nx, c = e - q * p.nx;
-    sg[e] = p.g[(long long)(r0 + q) * p.ld + PADL + c];
+    sg[e] = p.g[(long long)(r0 + q + R) * p.ld + PADL + c];   // g rows sit at offset H = R
   }
   __syncthreads();
 

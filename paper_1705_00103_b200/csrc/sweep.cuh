@@ -59,7 +59,10 @@ struct SweepParams {
   long long ld;                // pitch of every internal buffer, doubles
   long long units;             // nstrips * nrows
   int nx;                      // interior columns
-  int rows;                    // interior rows of this (slab) buffer (ghost test)
+  int rows;                    // interior rows of this (slab) buffer
+  int H;                       // ghost rows stored above / below the slab (buf and g)
+  int row_lo, row_hi;          // local rows that are interior in the GLOBAL grid
+                               // (others are Dirichlet ghosts: pass-through)
   int row0, nrows;             // the band of output rows of this launch
   int stages;                  // TMA ring depth
   int advance;                 // the last CTA advances n / flips cur (last launch of a sweep)
@@ -324,7 +327,7 @@ __device__ __forceinline__ void consumer_segment(ConsumerState<Point<STENCIL>::R
       const int nin = jb - ja + 2 * K * R;
       const int nsteps = nin + K - 1;
       const int row_base = ja - K * R;               // global row of input step 0
-      double* outp = dst + (long long)(ja + R) * ld + PADL + ca;
+      double* outp = dst + (long long)(ja + p.H) * ld + PADL + ca;
       for (int k0 = 0; k0 < nsteps; k0 += P) {
 #pragma unroll
         for (int ph = 0; ph < P; ++ph) {
@@ -390,7 +393,7 @@ __device__ __forceinline__ void consumer_segment(ConsumerState<Point<STENCIL>::R
                   ya[q] = cs.h2a[l][sl]; yb[q] = cs.h2b[l][sl];
                 }
                 const int G = row_base + kk - (l + 1) * R - l;   // global row of the output
-                const bool rowin = (unsigned)G < (unsigned)rows;
+                const bool rowin = G >= p.row_lo && G < p.row_hi;
                 const double Ja = Point<STENCIL>::jacobi_target(wa, xa, ya, ga);
                 const double Jb = Point<STENCIL>::jacobi_target(wb, xb, yb, gb);
                 const double da = __dsub_rn(Ja, wa[R]);
@@ -490,17 +493,17 @@ cjm_sweep_kernel(const SweepParams p) {
         for (int k = 0; k < nin; ++k) {
           if (used >= p.stages) mbar_wait(&empty[stage], phase ^ 1u);
           const int gin = ja - K * R + k;          // global row of the u row
-          const bool hasu = gin >= -R && gin < rows + R;
+          const bool hasu = gin >= -p.H && gin < rows + p.H;
           const int g1 = gin - R;                   // level-1 output row
-          const bool hasg = k >= 2 * R && g1 >= 0 && g1 < rows && gbytes;
+          const bool hasg = k >= 2 * R && g1 >= p.row_lo && g1 < p.row_hi && gbytes;
           mbar_arrive_expect_tx(&full[stage], (hasu ? ubytes : 0u) + (hasg ? gbytes : 0u));
           if (hasu)
             tma_row_load(su + (size_t)stage * ROW,
-                         src + (long long)(gin + R) * ld + (PADL - 2) + c0, ubytes,
+                         src + (long long)(gin + p.H) * ld + (PADL - 2) + c0, ubytes,
                          &full[stage], pol);
           if (hasg)
             tma_row_load(sg + (size_t)stage * T + (gc0 - c0),
-                         p.g + (long long)g1 * ld + PADL + gc0, gbytes, &full[stage], pol);
+                         p.g + (long long)(g1 + p.H) * ld + PADL + gc0, gbytes, &full[stage], pol);
           ++used;
           if (++stage == p.stages) { stage = 0; phase ^= 1u; }
         }
@@ -519,7 +522,7 @@ cjm_sweep_kernel(const SweepParams p) {
       const int c0 = strip * TOUT - E;
       // FAST: every row the segment touches is interior and the tile holds no
       // ghost / padding column, so no node of it is pass-through
-      const bool fast = ja - K * R >= 0 && jb + K * R <= rows && c0 >= 0 && c0 + T <= p.nx;
+      const bool fast = ja - K * R >= p.row_lo && jb + K * R <= p.row_hi && c0 >= 0 && c0 + T <= p.nx;
       if (fast)
         consumer_segment<STENCIL, NT, K, REDUCE, STORE, true>(cs, p, su, sg, lb, dst, ja, jb, c0,
                                                                tid, lane, acc_s, acc_m);
@@ -595,14 +598,14 @@ cjm_sweep_kernel(const SweepParams p) {
 // error"), NaN-propagating.  The maximum of non-negative doubles is
 // the maximum of their bit patterns, so one atomicMax per warp on the bits is
 // exact and order-free.
-__global__ void cjm_error_kernel(const double* buf, long long ld, int R, const double* ref,
+__global__ void cjm_error_kernel(const double* buf, long long ld, int H, const double* ref,
                                  long long ld_ref, int nx, int rows, unsigned long long* out_bits) {
   const long long total = (long long)nx * rows;
   double m = 0.0;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long j = e / nx, i = e - j * nx;
-    const double d = fabs(__dsub_rn(buf[(j + R) * ld + PADL + i], ref[j * ld_ref + i]));
+    const double d = fabs(__dsub_rn(buf[(j + H) * ld + PADL + i], ref[j * ld_ref + i]));
     m = nan_max(m, d);
   }
 #pragma unroll

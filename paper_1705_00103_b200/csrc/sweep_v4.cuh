@@ -127,7 +127,7 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
       g[0] = ga.x; g[1] = ga.y; g[2] = gb.x; g[3] = gb.y;
     }
     const int G = ls.row_base + kk - (l + 1) * R;           // global row of the output
-    const bool rowin = (unsigned)G < (unsigned)p.rows;
+    const bool rowin = G >= p.row_lo && G < p.row_hi;
     double o[4], dd[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -215,7 +215,7 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws
   ls.jb = jb;
   ls.row_base = ja - K * R;
   ls.uoff = wbase + 4 * lane;                        // shared index of column cl - 2
-  ls.outp = dst + (long long)(ja + R) * p.ld + PADL + cl;
+  ls.outp = dst + (long long)(ja + p.H) * p.ld + PADL + cl;
   const int nin = jb - ja + 2 * K * R;
   if (c0 + wbase >= p.nx + R) {
     // the whole warp window lies right of the last ghost column (ragged last
@@ -322,16 +322,16 @@ cjm_sweep_kernel_v4(const SweepParams p) {
         for (int k = 0; k < nin; ++k) {
           if (used >= p.stages) mbar_wait_a(empty_a + 8u * stage, phase ^ 1u);
           const int gin = ja - K * R + k;
-          const bool hasu = gin >= -R && gin < rows + R;
+          const bool hasu = gin >= -p.H && gin < rows + p.H;
           const int g1 = gin - R;
-          const bool hasg = k >= 2 * R && g1 >= 0 && g1 < rows && gbytes;
+          const bool hasg = k >= 2 * R && g1 >= p.row_lo && g1 < p.row_hi && gbytes;
           mbar_arrive_expect_tx(&full[stage], (hasu ? ubytes : 0u) + (hasg ? gbytes : 0u));
           if (hasu)
             tma_row_load(su + (size_t)stage * TG_::ROW,
-                         src + (long long)(gin + R) * ld + (PADL - 2) + c0, ubytes, &full[stage], pol);
+                         src + (long long)(gin + p.H) * ld + (PADL - 2) + c0, ubytes, &full[stage], pol);
           if (hasg)
             tma_row_load(sg + (size_t)stage * TG_::GROW + (gc0 - c0),
-                         p.g + (long long)g1 * ld + PADL + gc0, gbytes, &full[stage], pol);
+                         p.g + (long long)(g1 + p.H) * ld + PADL + gc0, gbytes, &full[stage], pol);
           ++used;
           if (++stage == p.stages) { stage = 0; phase ^= 1u; }
         }
@@ -362,7 +362,8 @@ cjm_sweep_kernel_v4(const SweepParams p) {
       // FAST per warp: its window holds no ghost / padding column and the
       // segment touches no ghost row
       const int cw = c0 + warp * WG::WOUT;
-      const bool fast = ja - K * R >= 0 && jb + K * R <= rows && cw >= 0 && cw + WG::WSPAN <= p.nx;
+      const bool fast = ja - K * R >= p.row_lo && jb + K * R <= p.row_hi && cw >= 0 &&
+                        cw + WG::WSPAN <= p.nx;
       if (fast)
         warp_segment<STENCIL, NW, K, REDUCE, STORE, true>(ws, p, su, sg, dst, ja, jb, c0, warp, lane,
                                                           acc_s, acc_m);

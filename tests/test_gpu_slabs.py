@@ -75,6 +75,56 @@ def test_slabs_bitwise_equal_single_domain(world, stencil, nx, ny, band_split):
         p.close()
 
 
+@pytest.mark.parametrize("world,stencil,nx,ny", [(2, 9, 300, 257), (4, 17, 130, 97), (3, 5, 200, 64),
+                                                 (8, 9, 513, 200)])
+@pytest.mark.parametrize("K,variant", [(2, 0), (3, 3), (2, 3), (4, 0)])
+@pytest.mark.parametrize("band_split", (0, 1))
+def test_deep_halo_slabs_bitwise(world, stencil, nx, ny, K, variant, band_split):
+    """K sweeps fused per launch across slabs: H = K r deep halos (u with H
+    ghost rows, rhs with H extra rows, refreshed after every launch), the
+    ghost rows inside the global grid computed redundantly, bitwise equal to
+    the whole-domain oracle."""
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=31)
+    nsweeps = 12
+    plans = []
+    for g in range(world):
+        kw = dict(world_size=world, rank=g, external_halo=1, temporal_k=K, band_split=band_split)
+        if variant:
+            kw["variant"] = variant
+        if stencil == 17 and variant == 0:
+            kw["variant"] = 3
+        plans.append(cjm.Plan(stencil, nx, ny, h, 1e-8, **kw))
+    H = plans[0].ghost_rows
+    if plans[0].info()["temporal_k"] != K:
+        pytest.skip("slabs too thin for this K (plan fell back to K=1)")
+    assert H == K * r and plans[0].rhs_ghost_rows == H
+    u_pad = np.pad(u0, ((H - r, H - r), (0, 0)))
+    b_pad = np.pad(b, ((H, H), (0, 0)))
+    us, bs, msgs = [], [], []
+    for g in range(world):
+        y0, nyl = cjm.cjm_slab(ny, world, g)
+        us.append(torch.from_numpy(u_pad[y0:y0 + nyl + 2 * H].copy()).cuda())
+        bs.append(torch.from_numpy(b_pad[y0:y0 + nyl + 2 * H].copy()).cuda())
+        msgs.append(cjm.cjm_halo_plan(ny, H, world, g))
+    for k in range(0, nsweeps, K):
+        for g in range(world):
+            plans[g].sweeps(bs[g], us[g], k, K)
+        staged = []
+        for g in range(world):
+            for m in msgs[g]:
+                staged.append((m["peer"], g, us[g][m["send_row"]:m["send_row"] + m["rows"]].clone()))
+        for peer, src, blk in staged:
+            m = [x for x in msgs[peer] if x["peer"] == src][0]
+            us[peer][m["recv_row"]:m["recv_row"] + m["rows"]] = blk
+    field = torch.cat([us[g][H:-H] for g in range(world)]).cpu().numpy()
+    s_ = oracle.schedule(stencil, nx, ny, 1e-8)
+    uo = oracle.sweeps(stencil, u0, oracle.rhs_to_g(stencil, h, b), s_["w"], 0, nsweeps)
+    assert np.array_equal(field, uo[r:-r])
+    for p_ in plans:
+        p_.close()
+
+
 def test_external_halo_plan_refuses_solve():
     u0, b, h = inputs.test_problem(64, 64, 1)
     with cjm.Plan(9, 64, 64, h, 1e-8, world_size=2, rank=0, external_halo=1) as plan:
