@@ -38,7 +38,7 @@ def test_slabs_bitwise_equal_single_domain(world, stencil, nx, ny, band_split):
     for g in range(world):
         y0, nyl = cjm.cjm_slab(ny, world, g)
         plans.append(cjm.Plan(stencil, nx, ny, h, 1e-8, world_size=world, rank=g, external_halo=1,
-                              band_split=band_split))
+                              band_split=band_split, temporal_k=1))
         assert (plans[-1].y0, plans[-1].ny_local) == (y0, nyl)
         us.append(torch.from_numpy(u0[y0:y0 + nyl + 2 * r].copy()).cuda())
         bs.append(torch.from_numpy(b[y0:y0 + nyl].copy()).cuda())
@@ -127,7 +127,7 @@ def test_deep_halo_slabs_bitwise(world, stencil, nx, ny, K, variant, band_split)
 
 def test_external_halo_plan_refuses_solve():
     u0, b, h = inputs.test_problem(64, 64, 1)
-    with cjm.Plan(9, 64, 64, h, 1e-8, world_size=2, rank=0, external_halo=1) as plan:
+    with cjm.Plan(9, 64, 64, h, 1e-8, world_size=2, rank=0, external_halo=1, temporal_k=1) as plan:
         y0, nyl = plan.y0, plan.ny_local
         with pytest.raises(cjm.CJMError) as e:
             plan.solve(torch.from_numpy(b[:nyl].copy()).cuda(),
