@@ -944,8 +944,9 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   // ---- buffers: (ny_local + 2R) rows of pitch ld; interior column 0 at PADL
   pl->ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
   pl->H = pl->world > 1 ? pl->K * R : R;
-  pl->Hu = (pl->world > 1 && opt.external_halo) ? pl->H : R;
-  pl->Hr = (pl->world > 1 && opt.external_halo) ? pl->H : 0;
+  const bool deep_external = pl->world > 1 && opt.external_halo && pl->K > 1;
+  pl->Hu = deep_external ? pl->H : R;
+  pl->Hr = deep_external ? pl->H : 0;
   pl->row_lo = std::max(-pl->H, -pl->y0);
   pl->row_hi = std::min(nyl + pl->H, ny - pl->y0);
   pl->buf_elems = (size_t)(nyl + 2 * pl->H) * pl->ld;
