@@ -111,29 +111,31 @@ KernelFn pick_nt(int NT, int K, int mode) {
   return NT == 256 ? pick_k<ST, 256>(K, mode) : pick_k<ST, 128>(K, mode);
 }
 
-// warp-tiled variant (sweep_v4.cuh), 4 consumer warps
-template <int ST, int K>
+// warp-tiled variant (sweep_v4.cuh), 4 consumer warps, C columns per lane
+template <int ST, int K, int C>
 KernelFn pick_mode_v4(int mode) {
   switch (mode) {
-    case MODE_HOT: return cjm::cjm_sweep_kernel_v4<ST, 4, K, false, true>;
-    case MODE_CHECK: return cjm::cjm_sweep_kernel_v4<ST, 4, K, true, true>;
-    default: return cjm::cjm_sweep_kernel_v4<ST, 4, 1, true, false>;
+    case MODE_HOT: return cjm::cjm_sweep_kernel_v4<ST, 4, K, C, false, true>;
+    case MODE_CHECK: return cjm::cjm_sweep_kernel_v4<ST, 4, K, C, true, true>;
+    default: return cjm::cjm_sweep_kernel_v4<ST, 4, 1, C, true, false>;
   }
 }
 
 // the 17-point warp-tiled kernel with K >= 2 does not fit the register file
 // (5-row rings of 4 columns x 3 arrays per level): not instantiated, the plan
 // uses the shared-line variant there
-template <int ST>
+template <int ST, int C>
 KernelFn pick_k_v4(int K, int mode) {
-  if constexpr (ST == 17) {
-    return K == 1 ? pick_mode_v4<ST, 1>(mode) : nullptr;
+  if constexpr (ST == 17 && C == 4) {
+    return K == 1 ? pick_mode_v4<ST, 1, C>(mode) : nullptr;
+  } else if constexpr (ST == 17) {
+    return K == 1 ? pick_mode_v4<ST, 1, C>(mode) : K == 2 ? pick_mode_v4<ST, 2, C>(mode) : nullptr;
   } else {
     switch (K) {
-      case 1: return pick_mode_v4<ST, 1>(mode);
-      case 2: return pick_mode_v4<ST, 2>(mode);
-      case 3: return pick_mode_v4<ST, 3>(mode);
-      default: return pick_mode_v4<ST, 4>(mode);
+      case 1: return pick_mode_v4<ST, 1, C>(mode);
+      case 2: return pick_mode_v4<ST, 2, C>(mode);
+      case 3: return pick_mode_v4<ST, 3, C>(mode);
+      default: return pick_mode_v4<ST, 4, C>(mode);
     }
   }
 }
@@ -141,9 +143,16 @@ KernelFn pick_k_v4(int K, int mode) {
 KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode) {
   if (variant == 4) {
     switch (stencil) {
-      case 5: return pick_k_v4<5>(K, mode);
-      case 9: return pick_k_v4<9>(K, mode);
-      default: return pick_k_v4<17>(K, mode);
+      case 5: return pick_k_v4<5, 4>(K, mode);
+      case 9: return pick_k_v4<9, 4>(K, mode);
+      default: return pick_k_v4<17, 4>(K, mode);
+    }
+  }
+  if (variant == 5) {   // warp-tiled, 2 columns per lane
+    switch (stencil) {
+      case 5: return pick_k_v4<5, 2>(K, mode);
+      case 9: return pick_k_v4<9, 2>(K, mode);
+      default: return pick_k_v4<17, 2>(K, mode);
     }
   }
   switch (stencil) {
@@ -215,21 +224,24 @@ struct cjm_plan_s {
 
 namespace {
 
-int v4_tout(int R, int K) {      // owned columns per CTA strip, warp-tiled variant
+int v4_cpl(int variant) { return variant == 5 ? 2 : 4; }
+
+int v4_tout(int R, int K, int C) {      // owned columns per CTA strip, warp-tiled variant
   const int E = K == 1 ? 0 : ((R * (K - 1) + 1) & ~1);
-  return 4 * (128 - 2 * E);
+  return 4 * (32 * C - 2 * E);
 }
 
 int tile_out(const cjm_plan_s* pl, int K) {
-  if (pl->variant == 4) return v4_tout(pl->R, K);
+  if (pl->variant >= 4) return v4_tout(pl->R, K, v4_cpl(pl->variant));
   return 2 * pl->NT - 2 * tile_e(pl->R, K);
 }
 
 size_t smem_bytes(const cjm_plan_s* pl, int K) {
-  if (pl->variant == 4) {
+  if (pl->variant >= 4) {
+    const int C = v4_cpl(pl->variant);
     const int E = K == 1 ? 0 : ((pl->R * (K - 1) + 1) & ~1);
-    const int WOUT = 128 - 2 * E;
-    const int TG = 3 * WOUT + 128;
+    const int WOUT = 32 * C - 2 * E;
+    const int TG = 3 * WOUT + 32 * C;
     const int ROW = (TG + 4 + 7) / 8 * 8, GROW = (TG + 7) / 8 * 8;
     return (size_t)pl->stages * (ROW + GROW) * sizeof(double) +
            2 * (size_t)pl->stages * sizeof(uint64_t);
@@ -240,7 +252,7 @@ size_t smem_bytes(const cjm_plan_s* pl, int K) {
          2 * (size_t)pl->stages * sizeof(uint64_t);
 }
 
-int block_threads(const cjm_plan_s* pl) { return pl->variant == 4 ? 4 * 32 + 32 : pl->NT + 32; }
+int block_threads(const cjm_plan_s* pl) { return pl->variant >= 4 ? 4 * 32 + 32 : pl->NT + 32; }
 
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur.
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur, over the
@@ -778,7 +790,8 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
       (opt.world_size > 1 && !opt.nccl_id && !opt.external_halo) ||
       (opt.method != CJM_METHOD_CHEBYSHEV && opt.method != CJM_METHOD_JACOBI) ||
       (opt.tile_w != 0 && opt.tile_w != 256 && opt.tile_w != 512) || opt.stages < 0 ||
-      opt.temporal_k < 0 || opt.temporal_k > 4 || (opt.variant != 0 && opt.variant != 3 && opt.variant != 4) ||
+      opt.temporal_k < 0 || opt.temporal_k > 4 ||
+      (opt.variant != 0 && opt.variant != 3 && opt.variant != 4 && opt.variant != 5) ||
       opt.stages > 32 || opt.ctas_per_sm < 0 || opt.graph_chunk < 0 || opt.max_cycles < 0 ||
       opt.jacobi_check < 0) {
     set_error("cjm_plan", "invalid argument");
@@ -858,20 +871,22 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   // multi-GPU: K-fused launches need H = K r deep halos, exchanged after every
   // launch; the slab must stay thicker than 2H + 1 rows (else fall back to K=1)
   if (pl->world > 1 && nyl < 2 * pl->K * R + 1) pl->K = 1;
-  if (stencil == 17 && pl->K > 1) {
-    if (opt.variant == 4) {
-      set_error("cjm_plan", "variant 4 supports the 17-point stencil with temporal_k = 1 only");
-      return fail(CJM_ERR_INVALID_ARG);
+  if (stencil == 17 && pl->K > 1 && pl->variant >= 4) {
+    if (pl->variant == 4 || pl->K > 2) {
+      if (opt.variant >= 4) {
+        set_error("cjm_plan", "warp-tiled variants run the 17-point with temporal_k <= 2 (variant 5) only");
+        return fail(CJM_ERR_INVALID_ARG);
+      }
+      pl->variant = 3;
     }
-    pl->variant = 3;
   }
-  pl->stages = opt.stages > 0 ? opt.stages : (pl->variant == 4 ? 8 : (pl->NT == 256 ? 12 : 4));
+  pl->stages = opt.stages > 0 ? opt.stages : (pl->variant >= 4 ? 8 : (pl->NT == 256 ? 12 : 4));
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
   // The grid is sized for the hot kernel (persistent: ctas_per_sm per SM, all
   // resident).  Check / residual / remainder kernels may need more registers;
   // they then run the same grid in more than one wave, which is correct
   // because no CTA ever waits for another.
-  if (pl->variant == 4 && pl->stages < (pl->K - 1) * R + 2) {
+  if (pl->variant >= 4 && pl->stages < (pl->K - 1) * R + 2) {
     // the warp-tiled kernel holds a slot for R(K-1) steps after reading it
     set_error("cjm_plan", "stages must be >= r(temporal_k-1) + 2 for variant 4");
     return fail(CJM_ERR_INVALID_ARG);

@@ -22,17 +22,17 @@
 
 namespace cjm {
 
-template <int R, int K>
+template <int R, int K, int C>
 struct WarpGeom {
-  static constexpr int CPL = 4;                               // columns per lane
+  static constexpr int CPL = C;                               // columns per lane (2 or 4)
   static constexpr int WSPAN = 32 * CPL;                      // warp window
   static constexpr int E = (K == 1) ? 0 : ((R * (K - 1) + 1) & ~1);
   static constexpr int WOUT = WSPAN - 2 * E;                  // owned per warp
 };
 
-template <int R, int K, int NW>
+template <int R, int K, int NW, int C>
 struct TileV4 {
-  using WG = WarpGeom<R, K>;
+  using WG = WarpGeom<R, K, C>;
   static constexpr int TOUT = NW * WG::WOUT;                  // owned per CTA strip
   static constexpr int TG = (NW - 1) * WG::WOUT + WG::WSPAN;  // g columns loaded
   static constexpr int TLOAD = TG + 4;                        // u columns loaded
@@ -40,10 +40,9 @@ struct TileV4 {
   static constexpr int GROW = ((TG + 7) / 8) * 8;
 };
 
-template <int R, int K>
+template <int R, int K, int C>
 struct WarpState {
   static constexpr int P = 2 * R + 1;
-  static constexpr int C = WarpGeom<R, K>::CPL;
   double u[K][P][C], h1[K][P][C], h2[K][P][C];   // ring slot = step mod P
   double wl[K];
   int stage;
@@ -51,28 +50,30 @@ struct WarpState {
   uint32_t full_a, empty_a;
 };
 
-// Push one row of level values (4 centre values + neighbours) into slot `sl`
-// of the level's ring: centre values and pair sums (west + east).
-template <int R, int K>
-__device__ __forceinline__ void push_row(WarpState<R, K>& ws, int l, int sl, const double (&c)[4],
+// Push one row of level values (C centre values + neighbours: l2, l1 west of
+// column 0, r1, r2 east of column C-1) into slot `sl` of the level's ring:
+// centre values and pair sums (west + east).
+template <int R, int K, int C>
+__device__ __forceinline__ void push_row(WarpState<R, K, C>& ws, int l, int sl, const double (&c)[C],
                                          double l2, double l1, double r1, double r2) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) ws.u[l][sl][j] = c[j];
-  ws.h1[l][sl][0] = __dadd_rn(l1, c[1]);
-  ws.h1[l][sl][1] = __dadd_rn(c[0], c[2]);
-  ws.h1[l][sl][2] = __dadd_rn(c[1], c[3]);
-  ws.h1[l][sl][3] = __dadd_rn(c[2], r1);
-  if (R == 2) {
-    ws.h2[l][sl][0] = __dadd_rn(l2, c[2]);
-    ws.h2[l][sl][1] = __dadd_rn(l1, c[3]);
-    ws.h2[l][sl][2] = __dadd_rn(c[0], r1);
-    ws.h2[l][sl][3] = __dadd_rn(c[1], r2);
+  for (int j = 0; j < C; ++j) {
+    ws.u[l][sl][j] = c[j];
+    const double w1 = j == 0 ? l1 : c[j - 1];
+    const double e1 = j == C - 1 ? r1 : c[j + 1];
+    ws.h1[l][sl][j] = __dadd_rn(w1, e1);
+    if (R == 2) {
+      const double w2 = j == 0 ? l2 : (j == 1 ? l1 : c[j - 2]);
+      const double e2 = j == C - 1 ? r2 : (j == C - 2 ? r1 : c[j + 2]);
+      ws.h2[l][sl][j] = __dadd_rn(w2, e2);
+    }
   }
 }
 
 // Per-segment constants of one lane.
+template <int C>
 struct LaneSeg {
-  bool in[4], own[4];
+  bool in[C], own[C];
   int ja, jb, row_base, uoff;
   double* outp;
 };
@@ -80,14 +81,14 @@ struct LaneSeg {
 // One step (input row kk, ring slot ph = kk mod P) of a lane: read the TMA row,
 // run every level (unconditionally: a level computes garbage until its window
 // is full, which is never stored), store the last level when it is active.
-template <int STENCIL, int NW, int K, bool REDUCE, bool STORE, bool FAST>
-__device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, LaneSeg& ls,
+template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE, bool FAST>
+__device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
                                           const SweepParams& p, const double* su, const double* sg,
                                           int kk, int ph, int lane, double& acc_s, double& acc_m) {
   constexpr int R = Point<STENCIL>::R;
   constexpr int P = 2 * R + 1;
-  using WG = WarpGeom<R, K>;
-  using TG_ = TileV4<R, K, NW>;
+  using WG = WarpGeom<R, K, C>;
+  using TG_ = TileV4<R, K, NW, C>;
   constexpr int E = WG::E;
   // ---- level 0 input: the TMA row of step kk (slot rs)
   // The slot of step kk stays held until level K-1 has read its g row, R(K-1)
@@ -96,41 +97,48 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
   const int rs = ws.stage;
   {
     mbar_wait_a(ws.full_a + 8u * rs, ws.phase);
-    const double* row = su + (size_t)rs * TG_::ROW + ls.uoff;
-    const double2 c01 = *reinterpret_cast<const double2*>(row + 2);
-    const double2 c23 = *reinterpret_cast<const double2*>(row + 4);
+    const double* row = su + (size_t)rs * TG_::ROW + ls.uoff;   // row[2 + j] = column j
+    double cc[C];
+#pragma unroll
+    for (int j = 0; j < C; j += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(row + 2 + j);
+      cc[j] = v.x;
+      cc[j + 1] = v.y;
+    }
     double l2 = 0.0, l1, r1, r2 = 0.0;
     if (R == 2) {
       const double2 lft = *reinterpret_cast<const double2*>(row);
-      const double2 rgt = *reinterpret_cast<const double2*>(row + 6);
+      const double2 rgt = *reinterpret_cast<const double2*>(row + 2 + C);
       l2 = lft.x; l1 = lft.y; r1 = rgt.x; r2 = rgt.y;
     } else {
       l1 = row[1];
-      r1 = row[6];
+      r1 = row[2 + C];
     }
     if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
-    const double cc[4] = {c01.x, c01.y, c23.x, c23.y};
-    push_row<R, K>(ws, 0, ph, cc, l2, l1, r1, r2);
+    push_row<R, K, C>(ws, 0, ph, cc, l2, l1, r1, r2);
   }
   // ---- levels, in order; level l hands its row to level l+1 in registers
 #pragma unroll
   for (int l = 0; l < K; ++l) {
     // g of level l's output row: arrived with the u row of step kk - lR
     // (stale during a level's warm-up: never stored then)
-    double g[4];
+    double g[C];
     {
       int gs = rs - l * R;
       if (gs < 0) gs += p.stages;
       const double* grow = sg + (size_t)gs * TG_::GROW + ls.uoff;
-      const double2 ga = *reinterpret_cast<const double2*>(grow);
-      const double2 gb = *reinterpret_cast<const double2*>(grow + 2);
-      g[0] = ga.x; g[1] = ga.y; g[2] = gb.x; g[3] = gb.y;
+#pragma unroll
+      for (int j = 0; j < C; j += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(grow + j);
+        g[j] = v.x;
+        g[j + 1] = v.y;
+      }
     }
     const int G = ls.row_base + kk - (l + 1) * R;           // global row of the output
     const bool rowin = G >= p.row_lo && G < p.row_hi;
-    double o[4], dd[4];
+    double o[C], dd[C];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < C; ++j) {
       double uw[P], x1[P], x2[P];
 #pragma unroll
       for (int q = 0; q < P; ++q) {                      // logical row q -> ring slot
@@ -146,37 +154,33 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
     const bool active = kk >= 2 * (l + 1) * R;
     if (REDUCE && l == 0 && active && (unsigned)(G - ls.ja) < (unsigned)(ls.jb - ls.ja)) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < C; ++j)
         if (ls.own[j]) { acc_s = __fma_rn(dd[j], dd[j], acc_s); acc_m = nan_max(acc_m, fabs(dd[j])); }
     }
     if (l + 1 < K) {
       // neighbours of this lane's columns at level l: adjacent lanes (the two
       // warp-edge lanes get their own values: garbage inside the lost halo)
-      const double l1 = __shfl_up_sync(0xffffffffu, o[3], 1);
+      const double l1 = __shfl_up_sync(0xffffffffu, o[C - 1], 1);
       const double r1 = __shfl_down_sync(0xffffffffu, o[0], 1);
       double l2 = 0.0, r2 = 0.0;
       if (R == 2) {
-        l2 = __shfl_up_sync(0xffffffffu, o[2], 1);
+        l2 = __shfl_up_sync(0xffffffffu, o[C - 2], 1);
         r2 = __shfl_down_sync(0xffffffffu, o[1], 1);
       }
-      push_row<R, K>(ws, l + 1, ph, o, l2, l1, r1, r2);
+      push_row<R, K, C>(ws, l + 1, ph, o, l2, l1, r1, r2);
     } else if (active) {
       if (STORE) {
-        // FAST: every column is interior, ownership depends on the lane only
-        // (E even: both columns of a pair are owned or neither)
-        const bool own01 = FAST ? (4 * lane >= E && 4 * lane + 2 <= WG::WSPAN - E)
-                                : (ls.own[0] && ls.own[1]);
-        const bool own23 = FAST ? (4 * lane + 2 >= E && 4 * lane + 4 <= WG::WSPAN - E)
-                                : (ls.own[2] && ls.own[3]);
-        if (own01) *reinterpret_cast<double2*>(ls.outp) = make_double2(o[0], o[1]);
-        else if (!FAST) {
-          if (ls.own[0]) ls.outp[0] = o[0];
-          if (ls.own[1]) ls.outp[1] = o[1];
-        }
-        if (own23) *reinterpret_cast<double2*>(ls.outp + 2) = make_double2(o[2], o[3]);
-        else if (!FAST) {
-          if (ls.own[2]) ls.outp[2] = o[2];
-          if (ls.own[3]) ls.outp[3] = o[3];
+#pragma unroll
+        for (int j = 0; j < C; j += 2) {
+          // FAST: every column is interior, ownership depends on the lane only
+          // (E even: both columns of a pair are owned or neither)
+          const bool ownp = FAST ? (C * lane + j >= E && C * lane + j + 2 <= WG::WSPAN - E)
+                                 : (ls.own[j] && ls.own[j + 1]);
+          if (ownp) *reinterpret_cast<double2*>(ls.outp + j) = make_double2(o[j], o[j + 1]);
+          else if (!FAST) {
+            if (ls.own[j]) ls.outp[j] = o[j];
+            if (ls.own[j + 1]) ls.outp[j + 1] = o[j + 1];
+          }
         }
       }
       ls.outp += p.ld;
@@ -192,29 +196,29 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K>& ws, L
   }
 }
 
-template <int STENCIL, int NW, int K, bool REDUCE, bool STORE, bool FAST>
-__device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws,
+template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE, bool FAST>
+__device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>& ws,
                                              const SweepParams& p, const double* su,
                                              const double* sg, double* dst, int ja, int jb,
                                              int c0, int warp, int lane, double& acc_s,
                                              double& acc_m) {
   constexpr int R = Point<STENCIL>::R;
   constexpr int P = 2 * R + 1;
-  using WG = WarpGeom<R, K>;
+  using WG = WarpGeom<R, K, C>;
   constexpr int E = WG::E;
   const int wbase = warp * WG::WOUT;                 // warp window offset in the tile
-  const int cl = c0 + wbase + 4 * lane;              // first column of this lane
-  LaneSeg ls;
+  const int cl = c0 + wbase + C * lane;              // first column of this lane
+  LaneSeg<C> ls;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < C; ++j) {
     const int c = cl + j;
     ls.in[j] = c >= 0 && c < p.nx;
-    ls.own[j] = ls.in[j] && (4 * lane + j) >= E && (4 * lane + j) < WG::WSPAN - E;
+    ls.own[j] = ls.in[j] && (C * lane + j) >= E && (C * lane + j) < WG::WSPAN - E;
   }
   ls.ja = ja;
   ls.jb = jb;
   ls.row_base = ja - K * R;
-  ls.uoff = wbase + 4 * lane;                        // shared index of column cl - 2
+  ls.uoff = wbase + C * lane;                        // shared index of column cl - 2
   ls.outp = dst + (long long)(ja + p.H) * p.ld + PADL + cl;
   const int nin = jb - ja + 2 * K * R;
   if (c0 + wbase >= p.nx + R) {
@@ -232,12 +236,14 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws
   for (; k0 + P <= nin; k0 += P) {                  // full periods: no guards
 #pragma unroll
     for (int ph = 0; ph < P; ++ph)
-      warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s, acc_m);
+      warp_step<STENCIL, NW, K, C, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s,
+                                                        acc_m);
   }
 #pragma unroll
   for (int ph = 0; ph < P - 1; ++ph)                 // tail
     if (k0 + ph < nin)
-      warp_step<STENCIL, NW, K, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s, acc_m);
+      warp_step<STENCIL, NW, K, C, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s,
+                                                        acc_m);
   // the last R(K-1) slots of the segment were still held: release them
   if (K > 1) {
     fence_proxy_async_smem();
@@ -258,12 +264,12 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K>& ws
 #ifndef V4_MIN_BLOCKS_K2
 #define V4_MIN_BLOCKS_K2 1
 #endif
-template <int STENCIL, int NW, int K, bool REDUCE, bool STORE>
-__global__ void __launch_bounds__(32 * NW + 32, (K == 2 ? V4_MIN_BLOCKS_K2 : 1))
+template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE>
+__global__ void __launch_bounds__(32 * NW + 32, (K == 2 && C == 4 ? V4_MIN_BLOCKS_K2 : 1))
 cjm_sweep_kernel_v4(const SweepParams p) {
   constexpr int R = Point<STENCIL>::R;
-  using WG = WarpGeom<R, K>;
-  using TG_ = TileV4<R, K, NW>;
+  using WG = WarpGeom<R, K, C>;
+  using TG_ = TileV4<R, K, NW, C>;
   constexpr int E = WG::E;
   constexpr int NT = 32 * NW;
 
@@ -340,14 +346,14 @@ cjm_sweep_kernel_v4(const SweepParams p) {
     }
   } else {
     // ---------------------------------------------- consumer warps
-    WarpState<R, K> ws;
+    WarpState<R, K, C> ws;
 #pragma unroll
     for (int l = 0; l < K; ++l) {
       ws.wl[l] = __ldg(p.w + (long long)((n + l) % (unsigned long long)p.P));
 #pragma unroll
       for (int q = 0; q < 2 * R + 1; ++q)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ws.u[l][q][j] = ws.h1[l][q][j] = ws.h2[l][q][j] = 0.0;
+        for (int j = 0; j < C; ++j) ws.u[l][q][j] = ws.h1[l][q][j] = ws.h2[l][q][j] = 0.0;
     }
     ws.stage = 0;
     ws.phase = 0;
@@ -365,11 +371,11 @@ cjm_sweep_kernel_v4(const SweepParams p) {
       const bool fast = ja - K * R >= p.row_lo && jb + K * R <= p.row_hi && cw >= 0 &&
                         cw + WG::WSPAN <= p.nx;
       if (fast)
-        warp_segment<STENCIL, NW, K, REDUCE, STORE, true>(ws, p, su, sg, dst, ja, jb, c0, warp, lane,
-                                                          acc_s, acc_m);
+        warp_segment<STENCIL, NW, K, C, REDUCE, STORE, true>(ws, p, su, sg, dst, ja, jb, c0, warp,
+                                                             lane, acc_s, acc_m);
       else
-        warp_segment<STENCIL, NW, K, REDUCE, STORE, false>(ws, p, su, sg, dst, ja, jb, c0, warp, lane,
-                                                           acc_s, acc_m);
+        warp_segment<STENCIL, NW, K, C, REDUCE, STORE, false>(ws, p, su, sg, dst, ja, jb, c0, warp,
+                                                              lane, acc_s, acc_m);
       uu = seg_end;
     }
   }

@@ -8,9 +8,9 @@ for line in sys.stdin:
     m = re.search(r"Compiling entry function '(\S+)'", line)
     if m:
         name = m.group(1)
-        k = re.search(r"cjm_sweep_kernel(_v4)?ILi(\d+)ELi(\d+)ELi(\d+)ELb([01])ELb([01])", name)
-        cur = (f"sweep{k.group(1) or ''}<{k.group(2)},{k.group(3)},K{k.group(4)},red{k.group(5)},st{k.group(6)}>"
-               if k else name[:40])
+        k = re.search(r"cjm_sweep_kernel(_v4)?ILi(\d+)ELi(\d+)ELi(\d+)E(?:Li(\d+)E)?Lb([01])ELb([01])", name)
+        cur = (f"sweep{k.group(1) or ''}<{k.group(2)},{k.group(3)},K{k.group(4)},C{k.group(5) or '-'},"
+               f"red{k.group(6)},st{k.group(7)}>" if k else name[:40])
         rows[cur] = {}
         continue
     if cur is None:

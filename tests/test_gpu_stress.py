@@ -20,7 +20,8 @@ if not torch.cuda.is_available():
 from paper_1705_00103_b200 import cjm  # noqa: E402
 
 
-@pytest.mark.parametrize("variant,K,stages", [(4, 1, 2), (4, 2, 3), (4, 3, 4), (3, 1, 2), (4, 1, 4)])
+@pytest.mark.parametrize("variant,K,stages", [(4, 1, 2), (4, 2, 3), (4, 3, 4), (3, 1, 2), (4, 1, 4),
+                                              (5, 2, 3)])
 def test_ring_reuse_is_race_free(variant, K, stages):
     n, cnt, trials = 1024, 16, 60
     u0, b, h = inputs.test_problem(n, n, 1, init="random")
