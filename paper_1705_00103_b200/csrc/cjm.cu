@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 
@@ -173,6 +174,24 @@ __global__ void set_state_kernel(cjm::SweepState* st, unsigned long long n) {
 
 }  // namespace
 
+// NCCL communicator cache: plans created repeatedly with the same unique id
+// (one plan per solve, as bench.py does) reuse the communicator instead of
+// paying ncclCommInitRank each time.  cjm_pool_trim destroys them.
+namespace {
+struct CommKey {
+  unsigned char id[128];
+  int world, rank, device;
+  bool operator<(const CommKey& o) const {
+    if (world != o.world) return world < o.world;
+    if (rank != o.rank) return rank < o.rank;
+    if (device != o.device) return device < o.device;
+    return std::memcmp(id, o.id, sizeof(id)) < 0;
+  }
+};
+std::mutex g_comm_mu;
+std::map<CommKey, std::pair<ncclComm_t, int>> g_comms;   // comm, plans using it
+}  // namespace
+
 struct cjm_plan_s {
   // problem
   int stencil = 9, R = 1, nx = 0, ny = 0, y0 = 0, ny_local = 0;
@@ -187,6 +206,7 @@ struct cjm_plan_s {
   // distribution
   int world = 1, rank = 0, device = 0;
   ncclComm_t comm = nullptr;
+  bool owns_comm = false;   // comm not in the cache: destroyed with the plan
   // device memory
   long long ld = 0;
   size_t buf_elems = 0, g_elems = 0;
@@ -766,7 +786,13 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   if (p->res_halo) cjm::pool_free(p->device, p->res_halo_bytes, p->res_halo);
   if (p->res_flags) cjm::pool_free(p->device, (size_t)p->res_ctas * sizeof(unsigned int), p->res_flags);
   cjm::pool_free_host(2 * sizeof(double), p->result_host);
-  if (p->comm) ncclCommDestroy(p->comm);
+  if (p->comm && p->owns_comm) {
+    ncclCommDestroy(p->comm);
+  } else if (p->comm) {   // back to the communicator cache (destroyed by cjm_pool_trim)
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    for (auto& kv : g_comms)
+      if (kv.second.first == p->comm) kv.second.second -= 1;
+  }
   tt.mark("free");
   delete p;
   return CJM_OK;
@@ -1000,12 +1026,34 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   if (pl->world > 1 && !opt.external_halo) {
     ncclUniqueId id;
     std::memcpy(&id, opt.nccl_id, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&pl->comm, pl->world, id, pl->rank);
-    if (r != ncclSuccess) {
-      set_error("ncclCommInitRank", ncclGetErrorString(r));
-      return fail(CJM_ERR_NCCL);
+    CommKey key;
+    std::memcpy(key.id, opt.nccl_id, sizeof(key.id));
+    key.world = pl->world;
+    key.rank = pl->rank;
+    key.device = dev;
+    {
+      std::lock_guard<std::mutex> lk(g_comm_mu);
+      auto it = g_comms.find(key);
+      if (it != g_comms.end() && it->second.second == 0) {
+        pl->comm = it->second.first;
+        it->second.second = 1;
+      }
+    }
+    if (!pl->comm) {
+      ncclResult_t r = ncclCommInitRank(&pl->comm, pl->world, id, pl->rank);
+      if (r != ncclSuccess) {
+        set_error("ncclCommInitRank", ncclGetErrorString(r));
+        pl->comm = nullptr;
+        return fail(CJM_ERR_NCCL);
+      }
+      std::lock_guard<std::mutex> lk(g_comm_mu);
+      auto it = g_comms.find(key);
+      if (it == g_comms.end()) g_comms[key] = {pl->comm, 1};
+      // (a second live plan with the same id keeps its own, uncached comm)
+      else pl->owns_comm = true;
     }
   }
+
   PLAN_CUDA(cudaDeviceSynchronize());
 #undef PLAN_CUDA
   tt.mark("streams+nccl+sync");
@@ -1116,6 +1164,17 @@ const char* cjm_last_error(void) { return g_last_error.c_str(); }
 cjm_status cjm_pool_trim(long long* cached_bytes_before) {
   if (cached_bytes_before) *cached_bytes_before = (long long)cjm::pool_cached_bytes();
   cjm::pool_trim();
+  {
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    for (auto it = g_comms.begin(); it != g_comms.end();) {
+      if (it->second.second == 0) {
+        ncclCommDestroy(it->second.first);
+        it = g_comms.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
   return CJM_OK;
 }
 
