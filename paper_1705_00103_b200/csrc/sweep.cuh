@@ -90,18 +90,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_addr(bar);
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done) : "r"(a), "r"(parity) : "memory");
-  } while (!done);
-}
-
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
   // the retry loop lives inside the asm block: no C-level divergent loop, so
   // the compiler emits no convergence barrier around it
@@ -196,36 +184,6 @@ struct Point<17> {
            __fma_rn(c_coef[4], S2,
            __fma_rn(c_coef[5], S3,
            __fma_rn(c_coef[6], S4, g))));
-  }
-};
-
-// Per-level register window of one thread (its 2 columns a, b).
-template <int R>
-struct Window {
-  double ua[2 * R + 1], ub[2 * R + 1];
-  double h1a[2 * R + 1], h1b[2 * R + 1];
-  double h2a[2 * R + 1], h2b[2 * R + 1];
-  __device__ __forceinline__ void clear() {
-#pragma unroll
-    for (int q = 0; q < 2 * R + 1; ++q) ua[q] = ub[q] = h1a[q] = h1b[q] = h2a[q] = h2b[q] = 0.0;
-  }
-  // Push the newest row: centre values ca, cb and neighbours l2, l1 (columns
-  // a-2, a-1) and r1, r2 (columns b+1, b+2).  Pair sums are (west + east).
-  __device__ __forceinline__ void push(double ca, double cb, double l2, double l1, double r1,
-                                       double r2) {
-#pragma unroll
-    for (int q = 0; q < 2 * R; ++q) {
-      ua[q] = ua[q + 1]; ub[q] = ub[q + 1];
-      h1a[q] = h1a[q + 1]; h1b[q] = h1b[q + 1];
-      if (R == 2) { h2a[q] = h2a[q + 1]; h2b[q] = h2b[q + 1]; }
-    }
-    ua[2 * R] = ca; ub[2 * R] = cb;
-    h1a[2 * R] = __dadd_rn(l1, cb);     // u(a-1) + u(a+1)
-    h1b[2 * R] = __dadd_rn(ca, r1);     // u(b-1) + u(b+1)
-    if (R == 2) {
-      h2a[2 * R] = __dadd_rn(l2, r1);   // u(a-2) + u(a+2)
-      h2b[2 * R] = __dadd_rn(l1, r2);   // u(b-2) + u(b+2)
-    }
   }
 };
 
