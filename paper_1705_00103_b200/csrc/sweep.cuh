@@ -449,7 +449,7 @@ cjm_sweep_kernel(const SweepParams p) {
         const uint32_t gbytes = gcols > 0 ? (uint32_t)(((gcols + 1) & ~1) * 8) : 0u;
         const int nin = jb - ja + 2 * K * R;
         for (int k = 0; k < nin; ++k) {
-          if (used >= p.stages) mbar_wait(&empty[stage], phase ^ 1u);
+          if (used >= p.stages) mbar_wait_a(smem_addr(&empty[stage]), phase ^ 1u);
           const int gin = ja - K * R + k;          // global row of the u row
           const bool hasu = gin >= -p.H && gin < rows + p.H;
           const int g1 = gin - R;                   // level-1 output row
