@@ -956,6 +956,8 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
     const int rows_min = (nyl + nsm - 1) / nsm;
     int rows = std::max(rows_min, std::min(16, nyl));
     if (smem_for(rows) + 1024 > (size_t)smem_optin) rows = rows_min;
+    // the whole grid in ONE CTA when it fits: no handshakes at all
+    if (smem_for(nyl) + 1024 <= (size_t)smem_optin) rows = nyl;
     const int ctas = (nyl + rows - 1) / rows;
     const size_t smem = smem_for(rows);
     int occ_r = 0;
