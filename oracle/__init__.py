@@ -83,6 +83,13 @@ def lib():
                                    dp, C.c_long, dp, C.c_long, dp, C.c_long, C.POINTER(Report)]
         L.oracle_sweeps.argtypes = [C.c_int, C.c_int, C.c_int, dp, C.c_long, dp, C.c_long, dp,
                                     C.c_long, C.c_long, C.c_long]
+        L.oracle_mask_sweep.argtypes = [C.c_int, C.c_int, dp, C.c_long, dp, dp, dp, dp, dp, C.c_long,
+                                        dp, C.c_long, C.c_double, dp, C.c_long]
+        L.oracle_mask_residual.argtypes = [C.c_int, C.c_int, dp, C.c_long, dp, dp, dp, dp, dp, C.c_long,
+                                           dp, C.c_long, dp, dp]
+        L.oracle_mask_solve.argtypes = [C.c_int, C.c_int, dp, dp, dp, dp, dp, C.c_long, dp, C.c_long,
+                                        C.c_double, C.c_double, C.c_double, C.c_int, dp, C.c_long,
+                                        C.POINTER(Report)]
         L.oracle_num_threads.restype = C.c_int
         L.oracle_set_num_threads.argtypes = [C.c_int]
         _lib = L
@@ -211,6 +218,45 @@ def solve(stencil: int, h: float, tol: float, b: np.ndarray, u0: np.ndarray,
         wo, wp, wl = None, None, 0
     lib().oracle_solve(stencil, nx, ny, h, tol, max_cycles, _dp(b), nx, _dp(u), u.shape[1],
                        wp, wl, C.byref(rep))
+    return u, rep.as_dict()
+
+
+def _mask_args(mask):
+    cs = [np.ascontiguousarray(mask[k], dtype=np.float64) for k in ("W", "E", "S", "N", "C")]
+    return cs, [_dp(c) for c in cs]
+
+
+def mask_sweep(mask: dict, u: np.ndarray, b: np.ndarray, w: float) -> np.ndarray:
+    """One weighted Jacobi sweep with a generic 5-point mask (dict of per-node
+    coefficient arrays W, E, S, N, C, each ny x nx); u has one ghost ring."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    ny, nx = b.shape
+    keep, ps = _mask_args(mask)
+    out = u.copy()
+    lib().oracle_mask_sweep(nx, ny, _dp(u), u.shape[1], *ps, nx, _dp(b), nx, w, _dp(out), u.shape[1])
+    return out
+
+
+def mask_residual(mask: dict, u: np.ndarray, b: np.ndarray) -> tuple[float, float]:
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    ny, nx = b.shape
+    keep, ps = _mask_args(mask)
+    l2, li = C.c_double(), C.c_double()
+    lib().oracle_mask_residual(nx, ny, _dp(u), u.shape[1], *ps, nx, _dp(b), nx, C.byref(l2), C.byref(li))
+    return l2.value, li.value
+
+
+def mask_solve(mask: dict, b: np.ndarray, u0: np.ndarray, kmin: float, kmax: float, tol: float,
+               max_cycles: int = 8):
+    u = np.array(u0, dtype=np.float64, order="C", copy=True)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    ny, nx = b.shape
+    keep, ps = _mask_args(mask)
+    rep = Report()
+    lib().oracle_mask_solve(nx, ny, *ps, nx, _dp(b), nx, kmin, kmax, tol, max_cycles, _dp(u), u.shape[1],
+                            C.byref(rep))
     return u, rep.as_dict()
 
 

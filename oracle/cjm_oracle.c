@@ -446,6 +446,121 @@ int oracle_solve(int stencil, int nx, int ny, double h, double tol,
     return rep->status = status;
 }
 
+/* ---------------------------------------------------------------------------
+ * Generic 5-point masks (NEXT-4, tab:ste1 upper part, tab:ste2):
+ * per-node coefficients c_W, c_E, c_S, c_N, c_C (PDE units, row-major
+ * ny x nx, pitch ldc) -- "both the central node ... and each of its neighbors
+ * ... can have different numerical factors".  The Jacobi
+ * correction of node (i,j) (DESIGN R10, one fixed association):
+ *   a_k = -c_k / c_C,  g = b / c_C,
+ *   J = fma(a_W, uW, fma(a_E, uE, fma(a_S, uS, fma(a_N, uN, g)))),
+ *   d = J - uC,   u' = fma(w, d, uC),   r = c_C d.
+ * ------------------------------------------------------------------------- */
+void oracle_mask_sweep(int nx, int ny, const double *u, long ldu, const double *cW,
+                       const double *cE, const double *cS, const double *cN, const double *cC,
+                       long ldc, const double *b, long ldb, double w, double *out, long ldo)
+{
+    #pragma omp parallel for schedule(static)
+    for (int j = 1; j <= ny; j++) {
+        for (int i = 1; i <= nx; i++) {
+            long c = (long)j * ldu + i;          /* one ghost ring */
+            long k = (long)(j - 1) * ldc + (i - 1);
+            long kb = (long)(j - 1) * ldb + (i - 1);
+            double cc = cC[k];
+            double aW = -cW[k] / cc, aE = -cE[k] / cc, aS = -cS[k] / cc, aN = -cN[k] / cc;
+            double g = b[kb] / cc;
+            double J = fma(aW, u[c - 1], fma(aE, u[c + 1], fma(aS, u[c - ldu], fma(aN, u[c + ldu], g))));
+            out[(long)j * ldo + i] = fma(w, J - u[c], u[c]);
+        }
+    }
+}
+
+/* ||r||_2, ||r||_inf with r = c_C d (the residual in PDE units). */
+void oracle_mask_residual(int nx, int ny, const double *u, long ldu, const double *cW,
+                          const double *cE, const double *cS, const double *cN,
+                          const double *cC, long ldc, const double *b, long ldb,
+                          double *l2, double *linf)
+{
+    double *rs = (double *)malloc(sizeof(double) * (size_t)ny * 2);
+    #pragma omp parallel for schedule(static)
+    for (int j = 1; j <= ny; j++) {
+        double s = 0.0, m = 0.0;
+        for (int i = 1; i <= nx; i++) {
+            long k = (long)(j - 1) * ldc + (i - 1);
+            long c = (long)j * ldu + i;
+            double cc = cC[k];
+            double aW = -cW[k] / cc, aE = -cE[k] / cc, aS = -cS[k] / cc, aN = -cN[k] / cc;
+            double g = b[(long)(j - 1) * ldb + (i - 1)] / cc;
+            double J = fma(aW, u[c - 1], fma(aE, u[c + 1], fma(aS, u[c - ldu], fma(aN, u[c + ldu], g))));
+            double r = cc * (J - u[c]);
+            s = s + r * r;
+            double ar = fabs(r);
+            if (ar > m || ar != ar) m = ar;
+        }
+        rs[2 * (j - 1)] = s;
+        rs[2 * (j - 1) + 1] = m;
+    }
+    double s = 0.0, m = 0.0;
+    for (int j = 0; j < ny; j++) {
+        s = s + rs[2 * j];
+        if (rs[2 * j + 1] > m || rs[2 * j + 1] != rs[2 * j + 1]) m = rs[2 * j + 1];
+    }
+    free(rs);
+    *l2 = sqrt(s);
+    *linf = m;
+}
+
+/* The CJM with a generic mask and caller-supplied spectral bounds (there is
+ * no closed form off the Cartesian grid): M, P, ordering and
+ * weights exactly as for the Cartesian stencils, stop as in oracle_solve. */
+int oracle_mask_solve(int nx, int ny, const double *cW, const double *cE, const double *cS,
+                      const double *cN, const double *cC, long ldc, const double *b, long ldb,
+                      double kmin, double kmax, double tol, int max_cycles,
+                      double *u, long ldu, oracle_report *rep)
+{
+    memset(rep, 0, sizeof(*rep));
+    if (nx < 1 || ny < 1 || !(kmin > 0.0 && kmax > kmin) || !(tol > 0.0 && tol < 1.0))
+        return rep->status = OR_INVALID;
+    long m = oracle_m_min(kmin, kmax, tol);
+    int a, bb;
+    long P = oracle_cycle_len(m, &a, &bb);
+    rep->kappa_min = kmin; rep->kappa_max = kmax; rep->m_min = m; rep->cycle_len = P;
+    long *t = (long *)malloc(sizeof(long) * (size_t)P);
+    double *w = (double *)malloc(sizeof(double) * (size_t)P);
+    oracle_ordering(a, bb, t);
+    oracle_weights(kmin, kmax, P, t, w);
+    free(t);
+    long rows = ny + 2;
+    double *v = (double *)malloc(sizeof(double) * (size_t)rows * ldu);
+    memcpy(v, u, sizeof(double) * (size_t)rows * ldu);
+    double l2, li;
+    oracle_mask_residual(nx, ny, u, ldu, cW, cE, cS, cN, cC, ldc, b, ldb, &l2, &li);
+    rep->r0_l2 = rep->r_l2 = l2;
+    rep->r0_linf = rep->r_linf = li;
+    int status = OR_NOT_CONVERGED;
+    if (l2 == 0.0) status = OR_OK;
+    double *cur = u, *nxt = v;
+    double rho_prev = l2;
+    for (int c = 1; status == OR_NOT_CONVERGED && c <= max_cycles; c++) {
+        for (long k = 0; k < P; k++) {
+            oracle_mask_sweep(nx, ny, cur, ldu, cW, cE, cS, cN, cC, ldc, b, ldb, w[k], nxt, ldu);
+            double *tmp = cur; cur = nxt; nxt = tmp;
+        }
+        rep->iterations += P;
+        rep->cycles = c;
+        oracle_mask_residual(nx, ny, cur, ldu, cW, cE, cS, cN, cC, ldc, b, ldb, &l2, &li);
+        rep->r_l2 = l2;
+        rep->r_linf = li;
+        if (!isfinite(l2)) { status = OR_DIVERGED; break; }
+        if (l2 <= tol * rep->r0_l2) { status = OR_OK; break; }
+        if (l2 > 0.5 * rho_prev) { status = OR_STAGNATED; break; }
+        rho_prev = l2;
+    }
+    if (cur != u) memcpy(u, cur, sizeof(double) * (size_t)rows * ldu);
+    free(v); free(w);
+    return rep->status = status;
+}
+
 int oracle_num_threads(void)
 {
 #ifdef _OPENMP
