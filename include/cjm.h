@@ -69,8 +69,15 @@ typedef enum {
     CJM_ERR_OOM = 8
 } cjm_status;
 
-/* The three Laplacians of the paper (value = number of points). */
-typedef enum { CJM_STENCIL_5 = 5, CJM_STENCIL_9 = 9, CJM_STENCIL_17 = 17 } cjm_stencil;
+/* The three Laplacians of the paper (value = number of points), and the
+ * generic per-node 5-point mask (tab:ste1 / tab:ste2; plans made
+ * with cjm_plan_mask only). */
+typedef enum {
+    CJM_STENCIL_MASK = 1,
+    CJM_STENCIL_5 = 5,
+    CJM_STENCIL_9 = 9,
+    CJM_STENCIL_17 = 17
+} cjm_stencil;
 
 /* Only Dirichlet data is covered by the paper's closed-form kappa bounds
  * (S:322).  Any other value -> CJM_ERR_UNSUPPORTED. */
@@ -171,6 +178,54 @@ cjm_status cjm_schedule(int stencil, int nx, int ny, double tol, int order,
  * rows), UNSUPPORTED (bc), OOM, CUDA, NCCL.  *out is NULL on error. */
 cjm_status cjm_plan(cjm_plan_t *out, int stencil, int nx, int ny, double h,
                     int bc, double tol, const cjm_options *opt);
+
+/* Generic 5-point masks (the code is "totally
+ * generic regarding discretization and coordinates", the Laplacian being a
+ * per-node mask of coefficients f_W, f_E, f_S, f_N, f_C, tab:ste1; tab:ste2
+ * lists the Cartesian, polar and bipolar ones).
+ *
+ * cjm_plan_mask: a single-GPU plan of nx x ny interior nodes whose operator
+ * is set afterwards by cjm_mask_set.  There is no closed form for the
+ * spectral bounds of D^-1 A off the Cartesian grid, so the caller passes them
+ * (0 < kappa_min < kappa_max; e.g. from cjm_mask_bounds or a dense
+ * eigensolver); M, P, the ordering and the weights then follow exactly as in
+ * cjm_schedule.  u keeps r = 1 ghost ring (the Dirichlet data), rhs is b in
+ * PDE units (A u = b with A the mask), residual norms are of b - A u.  One
+ * sweep per launch (options temporal_k / variant / tile_w / stages /
+ * resident / band_split are ignored; ctas_per_sm defaults to 8).
+ * Errors: INVALID_ARG (sizes, bounds, tol, options), UNSUPPORTED
+ * (world_size > 1), OOM, CUDA.  cjm_plan with CJM_STENCIL_MASK is
+ * INVALID_ARG. */
+cjm_status cjm_plan_mask(cjm_plan_t *out, int nx, int ny, double kappa_min,
+                         double kappa_max, double tol, const cjm_options *opt);
+
+/* Upload the mask of a cjm_plan_mask plan: five DEVICE arrays c_W, c_E, c_S,
+ * c_N, c_C (PDE units, ny x nx, row-major, pitch ld_c >= nx; node (i,j) at
+ * c[(j-1) ld_c + (i-1)]; W/E = first coordinate -/+, S/N = second -/+).  The
+ * plan stores a_q = -c_q / c_C (q = W, E, S, N; IEEE division) and c_C
+ * (DESIGN R10); the arrays are read during the call only (it synchronises
+ * cuda_stream) and stay owned by the caller.  c_C must be non-zero (a zero
+ * produces inf / NaN, reported as DIVERGED by the solve).  Must precede
+ * cjm_solve / cjm_sweeps / cjm_residual on the plan (else INVALID_ARG); may
+ * be called again to change the operator (kappa bounds stay those of the
+ * plan).  Errors: INVALID_ARG (not a mask plan, NULL array, ld_c < nx), CUDA. */
+cjm_status cjm_mask_set(cjm_plan_t p, const double *cW, const double *cE,
+                        const double *cS, const double *cN, const double *cC,
+                        long long ld_c, void *cuda_stream);
+
+/* Host-only estimate of the spectral bounds of D^-1 A for a 5-point mask
+ * (the numeric fallback; HOST arrays laid out as in
+ * cjm_mask_set).  The 5-point grid graph is bipartite, so the spectrum of
+ * D^-1 A = I - N is symmetric about 1: kappa_min = 1 - rho(N), kappa_max =
+ * 1 + rho(N), rho(N) by `iters` power-iteration steps (0 = 2000) from the
+ * positive smooth vector sin(pi i/(nx+1)) sin(pi j/(ny+1)).  An estimate:
+ * rho converges from below, so kappa_min may be slightly too large.  Cost
+ * iters x nx x ny on one host core.  Errors: INVALID_ARG (sizes, NULL, a zero
+ * or non-finite c_C, rho(N) >= 1: D^-1 A not positive definite). */
+cjm_status cjm_mask_bounds(int nx, int ny, const double *cW, const double *cE,
+                           const double *cS, const double *cN, const double *cC,
+                           long long ld_c, int iters, double *kappa_min,
+                           double *kappa_max);
 
 /* Static facts of a plan.  Any output pointer may be NULL.
  *   info: kappa_min/max, m_min, cycle_len (other fields zero) and plan_s.

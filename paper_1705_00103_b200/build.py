@@ -12,8 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcjm.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("cjm.cu", "schedule.cpp", "pool.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("sweep.cuh", "internal.h")] + \
+SOURCES = [os.path.join(CSRC, f) for f in ("cjm.cu", "schedule.cpp", "pool.cpp", "mask_bounds.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("sweep.cuh", "sweep_v4.cuh", "resident.cuh", "mask.cuh", "internal.h")] + \
     [os.path.join(ROOT, "include", "cjm.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

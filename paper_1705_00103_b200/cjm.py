@@ -7,7 +7,9 @@ of the library fails loudly.
 
 Names follow the C ABI: cjm_schedule, cjm_plan, cjm_plan_info, cjm_solve,
 cjm_solve_host, cjm_sweeps, cjm_residual, cjm_get_nccl_id, cjm_slab,
-cjm_plan_destroy.  The Plan class wraps a plan handle.
+cjm_plan_destroy, and for generic 5-point masks (NEXT-4) cjm_plan_mask,
+cjm_mask_set, cjm_mask_bounds.  The Plan / MaskPlan classes wrap a plan
+handle.
 """
 from __future__ import annotations
 
@@ -19,7 +21,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcjm.so")
 
-STENCIL_5, STENCIL_9, STENCIL_17 = 5, 9, 17
+STENCIL_MASK, STENCIL_5, STENCIL_9, STENCIL_17 = 1, 5, 9, 17
 BC_DIRICHLET = 0
 ORDER_LEBEDEV23, ORDER_ASCENDING = 0, 1
 METHOD_CHEBYSHEV, METHOD_JACOBI = 0, 1
@@ -32,7 +34,8 @@ STATUS = {0: "CJM_OK", 1: "CJM_ERR_INVALID_ARG", 2: "CJM_ERR_UNSUPPORTED",
 EXPORTS = ("cjm_default_options", "cjm_schedule", "cjm_plan", "cjm_plan_info", "cjm_solve",
            "cjm_solve_ref",
            "cjm_solve_host", "cjm_sweeps", "cjm_residual", "cjm_get_nccl_id", "cjm_slab", "cjm_halo_plan",
-           "cjm_plan_destroy", "cjm_pool_trim", "cjm_status_str", "cjm_last_error", "cjm_version")
+           "cjm_plan_destroy", "cjm_pool_trim", "cjm_status_str", "cjm_last_error", "cjm_version",
+           "cjm_plan_mask", "cjm_mask_set", "cjm_mask_bounds")
 
 
 class CJMError(RuntimeError):
@@ -91,6 +94,10 @@ def lib():
     L.cjm_schedule.argtypes = [i, i, i, C.c_double, i, dp, dp, C.POINTER(ll), C.POINTER(ll),
                                C.POINTER(ll), dp, ll]
     L.cjm_plan.argtypes = [C.POINTER(vp), i, i, i, C.c_double, i, C.c_double, C.POINTER(Options)]
+    L.cjm_plan_mask.argtypes = [C.POINTER(vp), i, i, C.c_double, C.c_double, C.c_double,
+                                C.POINTER(Options)]
+    L.cjm_mask_set.argtypes = [vp, vp, vp, vp, vp, vp, ll, vp]
+    L.cjm_mask_bounds.argtypes = [i, i, vp, vp, vp, vp, vp, ll, i, dp, dp]
     L.cjm_plan_info.argtypes = [vp, C.POINTER(Report), C.POINTER(i), C.POINTER(i), C.POINTER(i),
                                 C.POINTER(dp)]
     L.cjm_solve.argtypes = [vp, vp, ll, vp, ll, vp, C.POINTER(Report)]
@@ -207,6 +214,9 @@ class Plan:
             o.nccl_id = C.cast(self._id_buf, C.c_void_p)
         _check(lib().cjm_plan(C.byref(self._h), stencil, nx, ny, h, bc, tol, C.byref(o)), "cjm_plan")
         self.stencil, self.nx, self.ny, self.h, self.tol = stencil, nx, ny, h, tol
+        self._load_info()
+
+    def _load_info(self):
         info = self.info()
         self.reach, self.y0, self.ny_local = info["reach"], info["y0"], info["ny_local"]
         self.ghost_rows, self.rhs_ghost_rows = info["ghost_rows"], info["rhs_ghost_rows"]
@@ -296,6 +306,61 @@ class Plan:
 
     def __exit__(self, *a):
         self.close()
+
+
+MASK_KEYS = ("W", "E", "S", "N", "C")
+
+
+class MaskPlan(Plan):
+    """Owns a generic 5-point mask plan (cjm_plan_mask ... cjm_plan_destroy).
+    `mask` (optional): dict W, E, S, N, C of ny x nx float64 CUDA tensors,
+    passed to cjm_mask_set."""
+
+    def __init__(self, nx: int, ny: int, kappa_min: float, kappa_max: float, tol: float,
+                 mask: dict | None = None, **options):
+        self._h = C.c_void_p()
+        self._id_buf = None
+        o = cjm_default_options(**options)
+        _check(lib().cjm_plan_mask(C.byref(self._h), nx, ny, kappa_min, kappa_max, tol, C.byref(o)),
+               "cjm_plan_mask")
+        self.stencil, self.nx, self.ny, self.h, self.tol = STENCIL_MASK, nx, ny, 1.0, tol
+        self._load_info()
+        if mask is not None:
+            self.mask_set(mask)
+
+    def mask_set(self, mask: dict, stream=None) -> None:
+        ptrs, lds = [], set()
+        for k in MASK_KEYS:
+            t = mask[k]
+            if tuple(t.shape) != (self.ny, self.nx):
+                raise ValueError(f"mask[{k!r}]: shape {tuple(t.shape)}, plan expects {(self.ny, self.nx)}")
+            p, ld = _dev_ptr(t, f"mask[{k!r}]")
+            ptrs.append(p)
+            lds.add(ld)
+        if len(lds) != 1:
+            raise ValueError("mask arrays must share one pitch")
+        _check(lib().cjm_mask_set(self._h, *ptrs, lds.pop(), _stream(stream)), "cjm_mask_set")
+
+
+def cjm_plan_mask(nx, ny, kappa_min, kappa_max, tol=1e-8, mask=None, **options) -> MaskPlan:
+    return MaskPlan(nx, ny, kappa_min, kappa_max, tol, mask=mask, **options)
+
+
+def cjm_mask_set(plan: MaskPlan, mask: dict, stream=None) -> None:
+    plan.mask_set(mask, stream)
+
+
+def cjm_mask_bounds(mask: dict, iters: int = 0) -> tuple[float, float]:
+    """Host estimate (kappa_min, kappa_max) of D^-1 A for a mask of host
+    float64 arrays (cjm_mask_bounds: power iteration, bipartite symmetry)."""
+    arrs = [np.ascontiguousarray(mask[k], dtype=np.float64) for k in MASK_KEYS]
+    ny, nx = arrs[0].shape
+    if any(a.shape != (ny, nx) for a in arrs):
+        raise ValueError("mask arrays must share one shape")
+    kmin, kmax = C.c_double(), C.c_double()
+    _check(lib().cjm_mask_bounds(nx, ny, *[C.c_void_p(a.ctypes.data) for a in arrs], nx, iters,
+                                 C.byref(kmin), C.byref(kmax)), "cjm_mask_bounds")
+    return kmin.value, kmax.value
 
 
 def cjm_plan(stencil, nx, ny, h, bc=BC_DIRICHLET, tol=1e-8, **options) -> Plan:

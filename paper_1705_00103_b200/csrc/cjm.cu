@@ -11,6 +11,8 @@
 //                         host stop decision (row a8, DESIGN R4)
 //   multi-GPU           : NCCL halo exchange of r rows after every sweep (a9)
 //                         and sum/max allreduce of the reduction (a10)
+//   generic masks       : cjm_plan_mask + cjm_mask_set (NEXT-4): the same
+//                         executor with the per-node mask kernel (mask.cuh)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -29,6 +31,7 @@
 #include "sweep.cuh"
 #include "sweep_v4.cuh"
 #include "resident.cuh"
+#include "mask.cuh"
 
 namespace {
 
@@ -213,6 +216,10 @@ struct cjm_plan_s {
   double* buf[2] = {nullptr, nullptr};
   double* G = nullptr;
   double* w_dev = nullptr;
+  // generic 5-point mask (NEXT-4): planes aW, aE, aS, aN, cC of ny x ld
+  double* A = nullptr;
+  size_t a_elems = 0;
+  int mask_ready = 0, bands = 1;
   double* partials = nullptr;
   double* result = nullptr;
   double* result_host = nullptr;  // pinned, 2 doubles
@@ -279,8 +286,38 @@ int block_threads(const cjm_plan_s* pl) { return pl->variant >= 4 ? 4 * 32 + 32 
 // output rows [row0, row0 + nrows) of the slab (default: all of them).  Only
 // a launch with advance = 1 moves the device-side n / cur (the last launch of
 // a sweep that is split into bands).
+cjm_status launch_mask(cjm_plan_s* pl, int mode, cudaStream_t st) {
+  cjm::MaskParams mp;
+  mp.buf[0] = pl->buf[0];
+  mp.buf[1] = pl->buf[1];
+  mp.g = pl->G;
+  mp.a = pl->A;
+  mp.plane = (long long)pl->a_elems / 5;
+  mp.w = pl->w_dev;
+  mp.state = pl->state;
+  mp.partials = pl->partials;
+  mp.result = pl->result;
+  mp.P = pl->P;
+  mp.ld = pl->ld;
+  mp.nx = pl->nx;
+  mp.rows = pl->ny_local;
+  mp.bands = pl->bands;
+  const long long strips = (pl->nx + cjm::MASK_NT - 1) / cjm::MASK_NT;
+  const int grid = (int)std::min<long long>(pl->nctas, strips * pl->bands);
+  switch (mode) {
+    case MODE_HOT: cjm::cjm_mask_kernel<false, true><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+    case MODE_CHECK: cjm::cjm_mask_kernel<true, true><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+    default: cjm::cjm_mask_kernel<true, false><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  pl->launches += 1;
+  if (mode != MODE_RESID) pl->host_cur ^= 1;
+  return CJM_OK;
+}
+
 cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int row0 = 0,
                         int nrows = -1, int advance = 1) {
+  if (pl->stencil == CJM_STENCIL_MASK) return launch_mask(pl, mode, st);   // K = 1, one band
   if (nrows < 0) nrows = pl->ny_local;
   cjm::SweepParams sp;
   sp.buf[0] = pl->buf[0];
@@ -532,7 +569,11 @@ cjm_status stage_in(cjm_plan_s* pl, const double* rhs, long long ld_rhs, const d
                                (size_t)pl->nx * sizeof(double), (size_t)grows, kind, st));
     const long long total = (long long)pl->nx * grows;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-    cjm::cjm_scale_kernel<<<blocks, 256, 0, st>>>(g0, pl->ld, pl->nx, grows, pl->gscale);
+    if (pl->stencil == CJM_STENCIL_MASK)   // g = b / c_C
+      cjm::cjm_mask_scale_kernel<<<blocks, 256, 0, st>>>(g0, pl->ld, pl->nx, grows,
+                                                         pl->A + 4 * (pl->a_elems / 5));
+    else
+      cjm::cjm_scale_kernel<<<blocks, 256, 0, st>>>(g0, pl->ld, pl->nx, grows, pl->gscale);
     CUDA_TRY(cudaGetLastError());
     pl->launches += 1;
     // NCCL plans with deep halos: the neighbours' g rows (once per solve)
@@ -553,7 +594,8 @@ cjm_status stage_out(cjm_plan_s* pl, int which, double* u, long long ld_u, cudaM
 
 bool check_layout(const cjm_plan_s* pl, const void* rhs, long long ld_rhs, const void* u,
                   long long ld_u) {
-  return pl && u && ld_u >= pl->nx + 2 * pl->R && (!rhs || ld_rhs >= pl->nx);
+  return pl && u && ld_u >= pl->nx + 2 * pl->R && (!rhs || ld_rhs >= pl->nx) &&
+         (pl->stencil != CJM_STENCIL_MASK || pl->mask_ready);   // cjm_mask_set first
 }
 
 double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
@@ -782,6 +824,7 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   cjm::pool_free(p->device, p->buf_elems * sizeof(double), p->buf[1]);
   cjm::pool_free(p->device, p->g_elems * sizeof(double), p->G);
   cjm::pool_free(p->device, (size_t)p->P * sizeof(double), p->w_dev);
+  if (p->A) cjm::pool_free(p->device, p->a_elems * sizeof(double), p->A);
   cjm::pool_free(p->device, p->small_bytes, p->small_block);
   if (p->res_halo) cjm::pool_free(p->device, p->res_halo_bytes, p->res_halo);
   if (p->res_flags) cjm::pool_free(p->device, (size_t)p->res_ctas * sizeof(unsigned int), p->res_flags);
@@ -798,8 +841,9 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   return CJM_OK;
 }
 
-cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int bc, double tol,
-                    const cjm_options* opt_in) {
+// cjm_plan / cjm_plan_mask.  bounds = {kappa_min, kappa_max} for masks.
+static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, double h, int bc,
+                              double tol, const cjm_options* opt_in, const double* bounds) {
   if (!out) return CJM_ERR_INVALID_ARG;
   *out = nullptr;
   const auto t0 = std::chrono::steady_clock::now();
@@ -810,7 +854,12 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
     set_error("cjm_plan", "only Dirichlet boundary conditions are supported");
     return CJM_ERR_UNSUPPORTED;
   }
-  const int R = cjm::stencil_reach(stencil);
+  const bool mask = stencil == CJM_STENCIL_MASK;
+  if (mask && opt.world_size != 1) {
+    set_error("cjm_plan_mask", "generic-mask plans are single-GPU");
+    return CJM_ERR_UNSUPPORTED;
+  }
+  const int R = mask ? 1 : cjm::stencil_reach(stencil);
   if (!R || nx < 4 || ny < 4 || !(h > 0.0) || !std::isfinite(h) || !(tol > 0.0 && tol < 1.0) ||
       opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size ||
       (opt.world_size > 1 && !opt.nccl_id && !opt.external_halo) ||
@@ -840,15 +889,17 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   pl->h = h;
   pl->tol = tol;
   // g = (h^2 / c_C) b, c_C = -4, -20/6, -300/72 (DESIGN R6)
-  pl->gscale = stencil == 5 ? -(h * h) * 0.25 : stencil == 9 ? -(h * h) * 0.3
-                                                             : -(h * h) * (72.0 / 300.0);
+  // (masks: g = b / c_C per node, the residual r = c_C d is already in PDE units)
+  pl->gscale = mask ? -1.0 : stencil == 5 ? -(h * h) * 0.25 : stencil == 9 ? -(h * h) * 0.3
+                                                                      : -(h * h) * (72.0 / 300.0);
   pl->method = opt.method;
   pl->world = opt.world_size;
   pl->rank = opt.rank;
 
-  if (!cjm::build_schedule(stencil, nx, ny, tol, opt.order, &pl->sched)) {
+  if (mask ? !cjm::build_schedule_bounds(bounds[0], bounds[1], tol, opt.order, &pl->sched)
+           : !cjm::build_schedule(stencil, nx, ny, tol, opt.order, &pl->sched)) {
     delete pl;
-    set_error("cjm_plan", "invalid order");
+    set_error("cjm_plan", mask ? "invalid order or kappa bounds" : "invalid order");
     return CJM_ERR_INVALID_ARG;
   }
   if (opt.method == CJM_METHOD_JACOBI) {
@@ -879,6 +930,26 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   int nsm = 0;
   PLAN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
 
+  int smem_optin = 0;
+  PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (mask) {
+    // one sweep per launch, 256-column strips x row bands, up to 8 CTAs / SM
+    pl->variant = 0;
+    pl->K = 1;
+    pl->NT = cjm::MASK_NT;
+    pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
+    pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 8;
+    int occ = 0;
+    PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, (const void*)cjm::cjm_mask_kernel<true, true>, cjm::MASK_NT, 0));
+    if (occ < 1) {
+      set_error("cjm_plan_mask", "mask kernel does not fit on an SM");
+      return fail(CJM_ERR_INVALID_ARG);
+    }
+    pl->nctas = nsm * std::min(occ, pl->ctas_per_sm);
+    const int strips = (nx + cjm::MASK_NT - 1) / cjm::MASK_NT;
+    pl->bands = std::max(1, std::min(nyl, pl->nctas / strips));
+  } else {
   // ---- launch configuration
   // defaults from the r01 tuning sweep on B200 (profiles/r01_v3b_tune.jsonl):
   // two sweeps fused per launch, 256-column tiles, 4-row TMA ring, 4 CTAs/SM
@@ -917,8 +988,6 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
     set_error("cjm_plan", "stages must be >= r(temporal_k-1) + 2 for variant 4");
     return fail(CJM_ERR_INVALID_ARG);
   }
-  int smem_optin = 0;
-  PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   if (smem_bytes(pl, pl->K) > (size_t)smem_optin - 2048) {
     set_error("cjm_plan", "TMA ring too deep for shared memory (lower stages)");
     return fail(CJM_ERR_INVALID_ARG);
@@ -943,10 +1012,11 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
     return fail(CJM_ERR_INVALID_ARG);
   }
   pl->nctas = nsm * std::min(occ_min, pl->ctas_per_sm);
+  }
 
   // ---- resident (shared-memory) hot path: single GPU, whole grid fits in the
   // SMs' shared memory with at least 16 rows per CTA
-  if (pl->world == 1 && opt.resident >= 0) {
+  if (pl->world == 1 && opt.resident >= 0 && !mask) {
     const int ldS = nx + 2 * R;
     auto smem_for = [&](int rows) {
       return ((size_t)2 * (rows + 2 * R) * ldS + (size_t)rows * nx) * sizeof(double);
@@ -1000,6 +1070,10 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   PLAN_CUDA(cudaMemset(pl->buf[0], 0, pl->buf_elems * sizeof(double)));
   PLAN_CUDA(cudaMemset(pl->buf[1], 0, pl->buf_elems * sizeof(double)));
   PLAN_CUDA(cudaMemset(pl->G, 0, pl->g_elems * sizeof(double)));
+  if (mask) {
+    pl->a_elems = 5 * (size_t)ny * pl->ld;
+    PLAN_CUDA(cjm::pool_alloc(dev, pl->a_elems * sizeof(double), (void**)&pl->A));
+  }
   tt.mark("field buffers");
   PLAN_CUDA(cjm::pool_alloc(dev, (size_t)pl->P * sizeof(double), (void**)&pl->w_dev));
   PLAN_CUDA(cudaMemcpy(pl->w_dev, pl->sched.w.data(), (size_t)pl->P * sizeof(double),
@@ -1061,6 +1135,60 @@ cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int 
   tt.mark("streams+nccl+sync");
   pl->plan_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = pl;
+  return CJM_OK;
+}
+
+cjm_status cjm_plan(cjm_plan_t* out, int stencil, int nx, int ny, double h, int bc, double tol,
+                    const cjm_options* opt) {
+  if (stencil == CJM_STENCIL_MASK) {
+    if (out) *out = nullptr;
+    set_error("cjm_plan", "generic masks use cjm_plan_mask");
+    return CJM_ERR_INVALID_ARG;
+  }
+  return plan_create(out, stencil, nx, ny, h, bc, tol, opt, nullptr);
+}
+
+cjm_status cjm_plan_mask(cjm_plan_t* out, int nx, int ny, double kappa_min, double kappa_max,
+                         double tol, const cjm_options* opt) {
+  if (!(kappa_min > 0.0 && kappa_max > kappa_min) || !std::isfinite(kappa_max)) {
+    if (out) *out = nullptr;
+    set_error("cjm_plan_mask", "need 0 < kappa_min < kappa_max < inf");
+    return CJM_ERR_INVALID_ARG;
+  }
+  const double bounds[2] = {kappa_min, kappa_max};
+  return plan_create(out, CJM_STENCIL_MASK, nx, ny, 1.0, CJM_BC_DIRICHLET, tol, opt, bounds);
+}
+
+cjm_status cjm_mask_set(cjm_plan_t p, const double* cW, const double* cE, const double* cS,
+                        const double* cN, const double* cC, long long ld_c, void* cuda_stream) {
+  if (!p || p->stencil != CJM_STENCIL_MASK || !cW || !cE || !cS || !cN || !cC || ld_c < p->nx) {
+    set_error("cjm_mask_set", "invalid argument (not a mask plan, NULL array or ld_c < nx)");
+    return CJM_ERR_INVALID_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const long long total = (long long)p->nx * p->ny;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  cjm::cjm_mask_prepare_kernel<<<blocks, 256, 0, st>>>(p->A, (long long)p->a_elems / 5, p->ld, cW, cE,
+                                                       cS, cN, cC, ld_c, p->nx, p->ny);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  p->mask_ready = 1;
+  return CJM_OK;
+}
+
+cjm_status cjm_mask_bounds(int nx, int ny, const double* cW, const double* cE, const double* cS,
+                           const double* cN, const double* cC, long long ld_c, int iters,
+                           double* kappa_min, double* kappa_max) {
+  double kmin = 0, kmax = 0;
+  if (!kappa_min || !kappa_max ||
+      !cjm::mask_spectral_bounds(nx, ny, cW, cE, cS, cN, cC, ld_c, iters > 0 ? iters : 2000, &kmin,
+                                 &kmax)) {
+    set_error("cjm_mask_bounds", "invalid argument, zero / non-finite c_C or rho(N) >= 1");
+    return CJM_ERR_INVALID_ARG;
+  }
+  *kappa_min = kmin;
+  *kappa_max = kmax;
   return CJM_OK;
 }
 

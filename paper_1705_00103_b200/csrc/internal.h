@@ -26,6 +26,12 @@ long long chebyshev_degree(double kmin, double kmax, double tol);
 long long smooth_cycle_length(long long m, int* a_out, int* b_out);
 std::vector<long long> lebedev23_order(int a, int b);
 bool build_schedule(int stencil, int nx, int ny, double tol, int order, Schedule* s);
+// the same from caller-given bounds (generic masks, NEXT-4)
+bool build_schedule_bounds(double kmin, double kmax, double tol, int order, Schedule* s);
+// host estimate of the spectral bounds of D^-1 A for a 5-point mask (mask_bounds.cpp)
+bool mask_spectral_bounds(int nx, int ny, const double* cW, const double* cE, const double* cS,
+                          const double* cN, const double* cC, long long ldc, int iters,
+                          double* kmin, double* kmax);
 
 // device-buffer cache (pool.cpp)
 cudaError_t pool_alloc(int device, size_t bytes, void** out);

@@ -1,0 +1,187 @@
+// sm_100a fp64 CJM sweep with a generic 5-point mask (
+// P:380-418, tab:ste1, tab:ste2).
+//
+// The paper's code takes the Laplacian as a per-node mask of coefficient
+// functions (f_W, f_E, f_S, f_N, f_C) so that any orthogonal coordinate system
+// (polar, bipolar, ...) runs through the same Jacobi kernel.  Here
+// the mask is stored once per plan, already divided by the centre
+// coefficient:  a_q = -c_q / c_C (q = W, E, S, N), plus c_C itself for the
+// residual, and g = b / c_C replaces b.  One sweep is then, per node,
+//     J  = fma(aW, uW, fma(aE, uE, fma(aS, uS, fma(aN, uN, g))))   (DESIGN R10)
+//     d  = J - uC,   u' = fma(w, d, uC)
+// and the residual of a check launch is r = c_C d (PDE units).
+//
+// Memory-bound streaming kernel: per node and sweep it reads u (8 B, the four
+// neighbours come from L1 / registers), the four a planes and g (40 B) and
+// writes u' (8 B): 56 B/LUP (64 B/LUP in check launches, + c_C).  Temporal
+// blocking would only save the 16 B of u traffic of the 56 (the coefficients
+// must be re-read every sweep), so the kernel runs one sweep per launch.
+// Each CTA owns one 256-column strip and a contiguous band of rows (grid =
+// strips x bands sized to the persistent CTA count): a thread walks down its
+// column keeping uS / uC / uN in registers; the W / E neighbours are loads of
+// the same row that the neighbouring lanes also issue (L1 hits).  Same
+// device-side n / cur / ticket protocol and fixed-order reduction as the
+// Cartesian kernels (sweep.cuh), so it runs inside the same CUDA graphs.
+#pragma once
+
+#include "sweep.cuh"
+
+namespace cjm {
+
+struct MaskParams {
+  double* buf[2];              // iterate buffers, one ghost ring (H = 1)
+  const double* g;             // g = b / c_C, same layout as buf
+  const double* a;             // planes aW, aE, aS, aN, cC: node (i, j) at q * plane + j * ld + PADL + i
+  long long plane;             // elements per plane
+  const double* w;             // weights in application order, P entries
+  SweepState* state;
+  double* partials;            // 2 doubles per CTA (REDUCE)
+  double* result;              // sum r^2, max |r|
+  long long P, ld;
+  int nx, rows;                // interior columns / rows
+  int bands;                   // row bands per column strip
+};
+
+constexpr int MASK_NT = 256;
+
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <bool REDUCE, bool STORE>
+__global__ void __launch_bounds__(MASK_NT) cjm_mask_kernel(const MaskParams p) {
+  constexpr int NW = MASK_NT / 32;
+  __shared__ double red_s[NW], red_m[NW];
+  __shared__ int is_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned long long n = __ldcg(&p.state->n);
+  const unsigned int cur = __ldcg(&p.state->cur);
+  const double* src = (cur & 1u) ? p.buf[1] : p.buf[0];
+  double* dst = (cur & 1u) ? p.buf[0] : p.buf[1];
+  const double w = __ldg(p.w + (long long)(n % (unsigned long long)p.P));
+  const long long ld = p.ld;
+  double acc_s = 0.0, acc_m = 0.0;
+
+  const int strips = (p.nx + MASK_NT - 1) / MASK_NT;
+  const long long units = (long long)strips * p.bands;
+  for (long long uu = blockIdx.x; uu < units; uu += gridDim.x) {
+    const int strip = (int)(uu % strips), band = (int)(uu / strips);
+    const int i = strip * MASK_NT + tid;
+    const int ja = (int)((long long)band * p.rows / p.bands);
+    const int jb = (int)((long long)(band + 1) * p.rows / p.bands);
+    if (i >= p.nx || ja >= jb) continue;
+    long long c = (long long)(ja + 1) * ld + PADL + i;   // buf / g index of node (i, ja)
+    const double* ak = p.a + (long long)ja * ld + PADL + i;
+    double uS = __ldg(src + c - ld), uC = __ldg(src + c);
+#pragma unroll 4
+    for (int j = ja; j < jb; ++j) {
+      const double uN = __ldg(src + c + ld);
+      const double uW = __ldg(src + c - 1), uE = __ldg(src + c + 1);
+      const double aW = ld_stream(ak), aE = ld_stream(ak + p.plane);
+      const double aS = ld_stream(ak + 2 * p.plane), aN = ld_stream(ak + 3 * p.plane);
+      const double g = ld_stream(p.g + c);
+      const double J = __fma_rn(aW, uW, __fma_rn(aE, uE, __fma_rn(aS, uS, __fma_rn(aN, uN, g))));
+      const double d = __dsub_rn(J, uC);
+      if (STORE) dst[c] = __fma_rn(w, d, uC);
+      if (REDUCE) {
+        const double r = __dmul_rn(ld_stream(ak + 4 * p.plane), d);
+        acc_s = __fma_rn(r, r, acc_s);
+        acc_m = nan_max(acc_m, fabs(r));
+      }
+      uS = uC;
+      uC = uN;
+      c += ld;
+      ak += ld;
+    }
+  }
+
+  if (REDUCE) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc_s = __dadd_rn(acc_s, __shfl_xor_sync(0xffffffffu, acc_s, o));
+      acc_m = nan_max(acc_m, __shfl_xor_sync(0xffffffffu, acc_m, o));
+    }
+    if (lane == 0) { red_s[warp] = acc_s; red_m[warp] = acc_m; }
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0, m = 0.0;
+      for (int q = 0; q < NW; ++q) { s = __dadd_rn(s, red_s[q]); m = nan_max(m, red_m[q]); }
+      p.partials[2 * blockIdx.x] = s;
+      p.partials[2 * blockIdx.x + 1] = m;
+    }
+  }
+
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int t = atomicAdd(&p.state->ticket, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    if (REDUCE) {
+      double s = 0.0, m = 0.0;
+      for (int b = tid; b < (int)gridDim.x; b += MASK_NT) {
+        s = __dadd_rn(s, __ldcg(p.partials + 2 * b));
+        m = nan_max(m, __ldcg(p.partials + 2 * b + 1));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+        m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      }
+      if (lane == 0) { red_s[warp] = s; red_m[warp] = m; }
+      __syncthreads();
+      if (tid == 0) {
+        s = 0.0; m = 0.0;
+        for (int q = 0; q < NW; ++q) { s = __dadd_rn(s, red_s[q]); m = nan_max(m, red_m[q]); }
+        p.result[0] = s;
+        p.result[1] = m;
+      }
+    }
+    if (tid == 0) {
+      if (STORE) {
+        p.state->n = n + 1ull;
+        p.state->cur = cur ^ 1u;
+      }
+      p.state->ticket = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// a_q = -c_q / c_C and c_C into the plan's planes (cjm_mask_set).  The user's
+// coefficient arrays are ny x nx of pitch ldc.
+__global__ void cjm_mask_prepare_kernel(double* a, long long plane, long long ld, const double* cW,
+                                        const double* cE, const double* cS, const double* cN,
+                                        const double* cC, long long ldc, int nx, int rows) {
+  const long long total = (long long)nx * rows;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long j = e / nx, i = e - j * nx;
+    const long long k = j * ldc + i;
+    const double cc = cC[k];
+    double* q = a + j * ld + PADL + i;
+    q[0] = __ddiv_rn(-cW[k], cc);
+    q[plane] = __ddiv_rn(-cE[k], cc);
+    q[2 * plane] = __ddiv_rn(-cS[k], cc);
+    q[3 * plane] = __ddiv_rn(-cN[k], cc);
+    q[4 * plane] = cc;
+  }
+}
+
+// g = b / c_C in place on the interior of the internal g buffer (row a5 for masks).
+__global__ void cjm_mask_scale_kernel(double* g, long long ld, int nx, int rows, const double* cC) {
+  const long long total = (long long)nx * rows;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long j = e / nx, i = e - j * nx;
+    double* q = g + j * ld + PADL + i;
+    *q = __ddiv_rn(*q, cC[j * ld + PADL + i]);
+  }
+}
+
+}  // namespace cjm

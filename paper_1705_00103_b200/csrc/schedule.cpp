@@ -102,8 +102,10 @@ std::vector<long long> lebedev23_order(int a, int b) {
   return cur;
 }
 
-bool build_schedule(int stencil, int nx, int ny, double tol, int order, Schedule* s) {
-  if (!spectral_bounds(stencil, nx, ny, &s->kmin, &s->kmax)) return false;
+bool build_schedule_bounds(double kmin, double kmax, double tol, int order, Schedule* s) {
+  if (!(kmin > 0.0 && kmax > kmin) || !std::isfinite(kmax)) return false;
+  s->kmin = kmin;
+  s->kmax = kmax;
   s->m_min = chebyshev_degree(s->kmin, s->kmax, tol);
   int a = 0, b = 0;
   s->P = smooth_cycle_length(s->m_min, &a, &b);
@@ -123,6 +125,12 @@ bool build_schedule(int stencil, int nx, int ny, double tol, int order, Schedule
     s->w[k] = 1.0 / (s->kmin + span * (sn * sn));
   }
   return true;
+}
+
+bool build_schedule(int stencil, int nx, int ny, double tol, int order, Schedule* s) {
+  double kmin = 0, kmax = 0;
+  if (!spectral_bounds(stencil, nx, ny, &kmin, &kmax)) return false;
+  return build_schedule_bounds(kmin, kmax, tol, order, s);
 }
 
 }  // namespace cjm
