@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (run here, no GPU needed).
 
-    python scripts/ncu_summary.py full  <report.ncu-rep> <out.json> [config] [lups_per_launch]
+    python scripts/ncu_summary.py full  <report.ncu-rep> <out.json> [config] [lups_per_launch] [algorithmic_bytes_per_lup=24]
     python scripts/ncu_summary.py launches <launches.csv> <out.json>
 """
 import csv
@@ -33,7 +33,7 @@ def scale(v, unit):
     return v * mult if mult else v
 
 
-def full(rep, out, config=None, lups=None):
+def full(rep, out, config=None, lups=None, bpl="24"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -60,8 +60,8 @@ def full(rep, out, config=None, lups=None):
         if lups:
             lups = float(lups)
             summ["avg"].update(lups_per_launch=lups, dram_bytes_per_lup=(rd + wr) / lups,
-                               algorithmic_bytes_per_lup=24.0,
-                               algorithmic_gbs=24.0 * lups / t / 1e9)
+                               algorithmic_bytes_per_lup=float(bpl),
+                               algorithmic_gbs=float(bpl) * lups / t / 1e9)
         if config:
             summ["config"] = config
     with open(out, "w") as f:
