@@ -32,21 +32,24 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and \
-            os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in DEPS):
-        return LIB
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str | None = None) -> str:
+    """Build the library; `defines`/`out` build a measurement variant (e.g.
+    ("CJM_V4_RELEASE=2",)) at another path -- never the product library."""
+    target = out or LIB
+    if not force and os.path.exists(target) and \
+            os.path.getmtime(target) >= max(os.path.getmtime(d) for d in DEPS):
+        return target
     inc, lib = nccl_dirs()
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
            "-Xcompiler", "-fPIC,-ffp-contract=off", "-fmad=false",
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *SOURCES, "-o", tmp,
+           *[f"-D{d}" for d in defines], *SOURCES, "-o", tmp,
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -19,7 +19,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcjm.so")
+# CJM_LIB selects a measurement build of the same library (build.build(out=...));
+# there is no other implementation to fall back to.
+LIB_PATH = os.environ.get("CJM_LIB") or os.path.join(HERE, "libcjm.so")
 
 STENCIL_MASK, STENCIL_5, STENCIL_9, STENCIL_17 = 1, 5, 9, 17
 BC_DIRICHLET = 0
