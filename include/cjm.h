@@ -110,11 +110,13 @@ typedef struct {
     /* tuning knobs, 0 = automatic */
     int temporal_k;        /* sweeps fused per kernel launch (temporal blocking,
                               SURVEY NEXT-1), 1..4; multi-GPU plans use 1 */
-    int variant;           /* sweep kernel: 3 = shared-line levels, 4 = warp-tiled
-                              (default); both bitwise identical */
+    int variant;           /* sweep kernel, all bitwise identical: 3 = shared-line
+                              levels; warp-tiled with 4 (4) or 2 (5) columns per
+                              lane and one input row per TMA ring stage, or with
+                              2r+1 rows per stage (6: 4 columns, 7: 2 columns) */
     int tile_w;            /* variant 3 only: tile columns per CTA, 256 or 512 */
     int ctas_per_sm;       /* resident CTAs per SM of the persistent sweep grid */
-    int stages;            /* depth of the TMA row ring */
+    int stages;            /* depth of the TMA ring (stages of 1 or 2r+1 rows) */
     int graph_chunk;       /* sweeps captured per CUDA graph */
     int resident;          /* hot sweeps of grids that fit in the SMs' shared memory run
                               as ONE cooperative launch per cycle with the grid resident

@@ -115,49 +115,53 @@ KernelFn pick_nt(int NT, int K, int mode) {
   return NT == 256 ? pick_k<ST, 256>(K, mode) : pick_k<ST, 128>(K, mode);
 }
 
-// warp-tiled variant (sweep_v4.cuh), 4 consumer warps, C columns per lane
-template <int ST, int K, int C>
+// warp-tiled variant (sweep_v4.cuh), 4 consumer warps, C columns per lane,
+// RPS input rows per TMA ring stage
+template <int ST, int K, int C, int RPS>
 KernelFn pick_mode_v4(int mode) {
   switch (mode) {
-    case MODE_HOT: return cjm::cjm_sweep_kernel_v4<ST, 4, K, C, false, true>;
-    case MODE_CHECK: return cjm::cjm_sweep_kernel_v4<ST, 4, K, C, true, true>;
-    default: return cjm::cjm_sweep_kernel_v4<ST, 4, 1, C, true, false>;
+    case MODE_HOT: return cjm::cjm_sweep_kernel_v4<ST, 4, K, C, false, true, RPS>;
+    case MODE_CHECK: return cjm::cjm_sweep_kernel_v4<ST, 4, K, C, true, true, RPS>;
+    default: return cjm::cjm_sweep_kernel_v4<ST, 4, 1, C, true, false, RPS>;
   }
 }
 
 // the 17-point warp-tiled kernel with K >= 2 does not fit the register file
 // (5-row rings of 4 columns x 3 arrays per level): not instantiated, the plan
 // uses the shared-line variant there
-template <int ST, int C>
+template <int ST, int C, int RPS>
 KernelFn pick_k_v4(int K, int mode) {
   if constexpr (ST == 17 && C == 4) {
-    return K == 1 ? pick_mode_v4<ST, 1, C>(mode) : nullptr;
+    return K == 1 ? pick_mode_v4<ST, 1, C, RPS>(mode) : nullptr;
   } else if constexpr (ST == 17) {
-    return K == 1 ? pick_mode_v4<ST, 1, C>(mode) : K == 2 ? pick_mode_v4<ST, 2, C>(mode) : nullptr;
+    return K == 1 ? pick_mode_v4<ST, 1, C, RPS>(mode)
+                  : K == 2 ? pick_mode_v4<ST, 2, C, RPS>(mode) : nullptr;
   } else {
     switch (K) {
-      case 1: return pick_mode_v4<ST, 1, C>(mode);
-      case 2: return pick_mode_v4<ST, 2, C>(mode);
-      case 3: return pick_mode_v4<ST, 3, C>(mode);
-      default: return pick_mode_v4<ST, 4, C>(mode);
+      case 1: return pick_mode_v4<ST, 1, C, RPS>(mode);
+      case 2: return pick_mode_v4<ST, 2, C, RPS>(mode);
+      case 3: return pick_mode_v4<ST, 3, C, RPS>(mode);
+      default: return pick_mode_v4<ST, 4, C, RPS>(mode);
     }
   }
 }
 
-KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode) {
-  if (variant == 4) {
-    switch (stencil) {
-      case 5: return pick_k_v4<5, 4>(K, mode);
-      case 9: return pick_k_v4<9, 4>(K, mode);
-      default: return pick_k_v4<17, 4>(K, mode);
-    }
+template <int C, int MULTI>   // MULTI: 2r+1 rows per ring stage
+KernelFn pick_st_v4(int stencil, int K, int mode) {
+  switch (stencil) {
+    case 5: return pick_k_v4<5, C, MULTI ? 3 : 1>(K, mode);
+    case 9: return pick_k_v4<9, C, MULTI ? 3 : 1>(K, mode);
+    default: return pick_k_v4<17, C, MULTI ? 5 : 1>(K, mode);
   }
-  if (variant == 5) {   // warp-tiled, 2 columns per lane
-    switch (stencil) {
-      case 5: return pick_k_v4<5, 2>(K, mode);
-      case 9: return pick_k_v4<9, 2>(K, mode);
-      default: return pick_k_v4<17, 2>(K, mode);
-    }
+}
+
+KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode) {
+  switch (variant) {      // warp-tiled: 4 / 2 columns per lane, 1 / 2r+1 rows per stage
+    case 4: return pick_st_v4<4, 0>(stencil, K, mode);
+    case 5: return pick_st_v4<2, 0>(stencil, K, mode);
+    case 6: return pick_st_v4<4, 1>(stencil, K, mode);
+    case 7: return pick_st_v4<2, 1>(stencil, K, mode);
+    default: break;
   }
   switch (stencil) {
     case 5: return pick_nt<5>(NT, K, mode);
@@ -251,7 +255,8 @@ struct cjm_plan_s {
 
 namespace {
 
-int v4_cpl(int variant) { return variant == 5 ? 2 : 4; }
+int v4_cpl(int variant) { return (variant == 5 || variant == 7) ? 2 : 4; }
+int v4_rps(int variant, int R) { return variant >= 6 ? 2 * R + 1 : 1; }   // rows per ring stage
 
 int v4_tout(int R, int K, int C) {      // owned columns per CTA strip, warp-tiled variant
   const int E = K == 1 ? 0 : ((R * (K - 1) + 1) & ~1);
@@ -270,7 +275,7 @@ size_t smem_bytes(const cjm_plan_s* pl, int K) {
     const int WOUT = 32 * C - 2 * E;
     const int TG = 3 * WOUT + 32 * C;
     const int ROW = (TG + 4 + 7) / 8 * 8, GROW = (TG + 7) / 8 * 8;
-    return (size_t)pl->stages * (ROW + GROW) * sizeof(double) +
+    return (size_t)pl->stages * v4_rps(pl->variant, pl->R) * (ROW + GROW) * sizeof(double) +
            2 * (size_t)pl->stages * sizeof(uint64_t);
   }
   const int T = 2 * pl->NT, ROW = T + 8;
@@ -866,7 +871,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
       (opt.method != CJM_METHOD_CHEBYSHEV && opt.method != CJM_METHOD_JACOBI) ||
       (opt.tile_w != 0 && opt.tile_w != 256 && opt.tile_w != 512) || opt.stages < 0 ||
       opt.temporal_k < 0 || opt.temporal_k > 4 ||
-      (opt.variant != 0 && opt.variant != 3 && opt.variant != 4 && opt.variant != 5) ||
+      (opt.variant != 0 && (opt.variant < 3 || opt.variant > 7)) ||
       opt.stages > 32 || opt.ctas_per_sm < 0 || opt.graph_chunk < 0 || opt.max_cycles < 0 ||
       opt.jacobi_check < 0) {
     set_error("cjm_plan", "invalid argument");
@@ -951,41 +956,48 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     pl->bands = std::max(1, std::min(nyl, pl->nctas / strips));
   } else {
   // ---- launch configuration
-  // defaults from the r01 tuning sweep on B200 (profiles/r01_v3b_tune.jsonl):
-  // two sweeps fused per launch, 256-column tiles, 4-row TMA ring, 4 CTAs/SM
-  // multi-GPU: one CTA slot per SM left free so the NCCL exchange kernels can
-  // run next to the persistent interior kernel
+  // up to 4 CTAs/SM (the register file usually allows 2); multi-GPU: one CTA
+  // slot per SM left free so the NCCL exchange kernels can run next to the
+  // persistent interior kernel
   pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : (opt.world_size > 1 ? 3 : 4);
-  // 5/9-point: warp-tiled kernel (4), two sweeps per launch.  17-point: one
-  // sweep per launch through the shared-line kernel with 512-column tiles
-  // (its 5-row windows make K >= 2 latency-bound: 423 vs 290 us per sweep at
-  // 8192^2, profiles/r01_tune17.jsonl).
+  // Default: the warp-tiled kernel with 2 columns per lane and 2r+1 rows per
+  // TMA stage (variant 7).  5/9-point: three sweeps per launch, four from
+  // 8192^2 up; 17-point: two (profiles/r01_v7_tune.jsonl: 31.3 us per 9-point
+  // sweep at 4096^2 vs 37.9 for variant 4 at K = 2; 443 vs 599 at 16384^2;
+  // 242 vs 290 per 17-point sweep at 8192^2 for variant 3 at K = 1).  An
+  // explicit tile_w selects the shared-line kernel (variant 3).
   const bool wide = stencil == 17;
-  pl->NT = opt.tile_w == 512 || (opt.tile_w == 0 && wide && opt.variant != 4) ? 256 : 128;
-  pl->variant = opt.variant ? opt.variant : (wide ? 3 : 4);
+  pl->NT = opt.tile_w == 512 || (opt.tile_w == 0 && wide) ? 256 : 128;
+  pl->variant = opt.variant ? opt.variant : (opt.tile_w ? 3 : 7);
   pl->band_split = opt.band_split;
-  pl->K = opt.temporal_k > 0 ? opt.temporal_k : (wide ? 1 : 2);
+  pl->K = opt.temporal_k > 0 ? opt.temporal_k
+                             : (wide ? 2 : ((long long)nx * ny >= 8192LL * 8192LL ? 4 : 3));
   // multi-GPU: K-fused launches need H = K r deep halos, exchanged after every
   // launch; the slab must stay thicker than 2H + 1 rows (else fall back to K=1)
   if (pl->world > 1 && nyl < 2 * pl->K * R + 1) pl->K = 1;
   if (stencil == 17 && pl->K > 1 && pl->variant >= 4) {
-    if (pl->variant == 4 || pl->K > 2) {
+    if (v4_cpl(pl->variant) == 4 || pl->K > 2) {
       if (opt.variant >= 4) {
-        set_error("cjm_plan", "warp-tiled variants run the 17-point with temporal_k <= 2 (variant 5) only");
+        set_error("cjm_plan", "warp-tiled variants run the 17-point with temporal_k <= 2 (variants 5, 7) only");
         return fail(CJM_ERR_INVALID_ARG);
       }
       pl->variant = 3;
     }
   }
-  pl->stages = opt.stages > 0 ? opt.stages : (pl->variant >= 4 ? 8 : (pl->NT == 256 ? 12 : 4));
+  pl->stages = opt.stages > 0 ? opt.stages
+                              : (pl->variant >= 6 ? (R == 1 ? 6 : 4)
+                                                  : pl->variant >= 4 ? 8 : (pl->NT == 256 ? 12 : 4));
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
   // The grid is sized for the hot kernel (persistent: ctas_per_sm per SM, all
   // resident).  Check / residual / remainder kernels may need more registers;
   // they then run the same grid in more than one wave, which is correct
   // because no CTA ever waits for another.
-  if (pl->variant >= 4 && pl->stages < (pl->K - 1) * R + 2) {
-    // the warp-tiled kernel holds a slot for R(K-1) steps after reading it
-    set_error("cjm_plan", "stages must be >= r(temporal_k-1) + 2 for variant 4");
+  if (pl->variant >= 4 &&
+      pl->stages < ((pl->K - 1) * R + v4_rps(pl->variant, R) - 1) / v4_rps(pl->variant, R) + 2) {
+    // the warp-tiled kernel holds a stage until level K-1 has read the g rows
+    // of its rows, R(K-1) rows later
+    set_error("cjm_plan", "stages must be >= ceil(r(temporal_k-1) / rows_per_stage) + 2 for the "
+                          "warp-tiled variants");
     return fail(CJM_ERR_INVALID_ARG);
   }
   if (smem_bytes(pl, pl->K) > (size_t)smem_optin - 2048) {

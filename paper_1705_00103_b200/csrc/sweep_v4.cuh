@@ -13,6 +13,11 @@
 //  * the price is a lost halo of E = r(K-1) (rounded up to even) columns per
 //    side per WARP (instead of per CTA): a warp owns 128 - 2E output columns
 //    and adjacent warp windows overlap by 2E columns.
+//  * a TMA ring stage holds RPS consecutive input rows (RPS = 1, or 2r+1 for
+//    variants 6 / 7): one mbarrier wait, one cross-proxy fence and one
+//    release per RPS rows, and the RPS rows of a stage are independent
+//    dependency chains at every level, which the compiler interleaves (the
+//    kernel is latency-bound: few warps per SM, long fp64 chains per row).
 // Everything else (pass-through ghosts, the FAST instantiation, the fixed
 // association of DESIGN R6, device-side n / cur, ticket, fixed-order
 // reduction) is as in sweep.cuh.
@@ -78,26 +83,28 @@ struct LaneSeg {
   double* outp;
 };
 
-// One step (input row kk, ring slot ph = kk mod P) of a lane: read the TMA row,
-// run every level (unconditionally: a level computes garbage until its window
-// is full, which is never stored), store the last level when it is active.
-template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE, bool FAST>
-__device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
-                                          const SweepParams& p, const double* su, const double* sg,
-                                          int kk, int ph, int lane, double& acc_s, double& acc_m) {
+// One input row kk (row RI of the ring stage `st`; ring slot ph = kk mod P) of
+// a lane, the stage already waited for: read the TMA row, run every level
+// (unconditionally: a level computes garbage until its window is full, which
+// is never stored), store the last level when it is active.  RI and PH are
+// compile-time, so every register-ring slot and every stage offset folds.
+template <int STENCIL, int NW, int K, int C, int RPS, int RI, int PH, bool REDUCE, bool STORE,
+          bool FAST>
+__device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
+                                         const SweepParams& p, const double* su, const double* sg,
+                                         int st, int kk, int lane, double& acc_s, double& acc_m) {
   constexpr int R = Point<STENCIL>::R;
   constexpr int P = 2 * R + 1;
+  constexpr int ph = PH;
   using WG = WarpGeom<R, K, C>;
   using TG_ = TileV4<R, K, NW, C>;
   constexpr int E = WG::E;
-  // ---- level 0 input: the TMA row of step kk (slot rs)
-  // The slot of step kk stays held until level K-1 has read its g row, R(K-1)
-  // steps later (level l reads the g row that arrived with step kk - lR), so
-  // g needs no register ring.
-  const int rs = ws.stage;
+  // ---- level 0 input: row RI of stage st
+  // A stage stays held until level K-1 has read the g rows of all its rows,
+  // R(K-1) rows later (level l reads the g row that arrived with input row
+  // kk - lR), so g needs no register ring.
   {
-    mbar_wait_a(ws.full_a + 8u * rs, ws.phase);
-    const double* row = su + (size_t)rs * TG_::ROW + ls.uoff;   // row[2 + j] = column j
+    const double* row = su + ((size_t)st * RPS + RI) * TG_::ROW + ls.uoff;   // row[2 + j] = column j
     double cc[C];
 #pragma unroll
     for (int j = 0; j < C; j += 2) {
@@ -114,7 +121,6 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K, C>& ws
       l1 = row[1];
       r1 = row[2 + C];
     }
-    if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
     push_row<R, K, C>(ws, 0, ph, cc, l2, l1, r1, r2);
   }
   // ---- levels, in order; level l hands its row to level l+1 in registers
@@ -124,9 +130,12 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K, C>& ws
     // (stale during a level's warm-up: never stored then)
     double g[C];
     {
-      int gs = rs - l * R;
+      // input row kk - lR: row GR of the stage GB stages back (compile-time)
+      const int GB = (l * R - RI + RPS - 1) / RPS;  // l R <= RI: 0 (folds: l unrolled)
+      const int GR = RI - l * R + GB * RPS;
+      int gs = st - GB;
       if (gs < 0) gs += p.stages;
-      const double* grow = sg + (size_t)gs * TG_::GROW + ls.uoff;
+      const double* grow = sg + ((size_t)gs * RPS + GR) * TG_::GROW + ls.uoff;
 #pragma unroll
       for (int j = 0; j < C; j += 2) {
         const double2 v = *reinterpret_cast<const double2*>(grow + j);
@@ -173,7 +182,9 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K, C>& ws
 #pragma unroll
         for (int j = 0; j < C; j += 2) {
           // FAST: every column is interior, ownership depends on the lane only
-          // (E even: both columns of a pair are owned or neither)
+          // (E even: both columns of a pair are owned or neither).  (Stores
+          // predicated inside inline PTX instead of branches measured slower:
+          // 32.2 vs 31.4 us per sweep, profiles/r01_v7_tune.jsonl.)
           const bool ownp = FAST ? (C * lane + j >= E && C * lane + j + 2 <= WG::WSPAN - E)
                                  : (ls.own[j] && ls.own[j + 1]);
           if (ownp) *reinterpret_cast<double2*>(ls.outp + j) = make_double2(o[j], o[j + 1]);
@@ -186,9 +197,34 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K, C>& ws
       ls.outp += p.ld;
     }
   }
-  // ---- release the slot whose last reader (level K-1's g) was this step
-  if (kk >= (K - 1) * R) {
-    int rel = rs - (K - 1) * R;
+}
+
+// Process ring stage `st` (input rows kk0 .. kk0 + RPS - 1; ring slot of row
+// kk0 is PH0): wait for it, run its rows (rows >= nin only in a segment's
+// last stage, when GUARD), then release the stage whose rows level K-1 has
+// now read for the last time.
+template <int STENCIL, int NW, int K, int C, int RPS, int PH0, bool GUARD, bool REDUCE,
+          bool STORE, bool FAST>
+__device__ __forceinline__ void warp_stage(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
+                                           const SweepParams& p, const double* su,
+                                           const double* sg, int s, int kk0, int nin, int lane,
+                                           double& acc_s, double& acc_m) {
+  constexpr int R = Point<STENCIL>::R;
+  constexpr int P = 2 * R + 1;
+  constexpr int HS = ((K - 1) * R + RPS - 1) / RPS;   // stages held after processing
+  const int st = ws.stage;
+  mbar_wait_a(ws.full_a + 8u * st, ws.phase);
+  if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
+#define CJM_V4_ROW(RI)                                                                         \
+  if (RI < RPS && (!GUARD || kk0 + RI < nin))                                                  \
+    warp_row<STENCIL, NW, K, C, RPS, (RI < RPS ? RI : 0), (PH0 + RI) % P, REDUCE, STORE, FAST>( \
+        ws, ls, p, su, sg, st, kk0 + RI, lane, acc_s, acc_m);
+  CJM_V4_ROW(0) CJM_V4_ROW(1) CJM_V4_ROW(2) CJM_V4_ROW(3) CJM_V4_ROW(4)
+#undef CJM_V4_ROW
+  static_assert(RPS <= 5, "rows per stage <= 5");
+  // ---- release stage s - HS: level K-1 has read its last g row
+  if (s >= HS) {
+    int rel = st - HS;
     if (rel < 0) rel += p.stages;
     fence_proxy_async_smem();   // my reads of the slot before its TMA refill
     __syncwarp();
@@ -196,7 +232,7 @@ __device__ __forceinline__ void warp_step(WarpState<Point<STENCIL>::R, K, C>& ws
   }
 }
 
-template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE, bool FAST>
+template <int STENCIL, int NW, int K, int C, int RPS, bool REDUCE, bool STORE, bool FAST>
 __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>& ws,
                                              const SweepParams& p, const double* su,
                                              const double* sg, double* dst, int ja, int jb,
@@ -221,10 +257,11 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
   ls.uoff = wbase + C * lane;                        // shared index of column cl - 2
   ls.outp = dst + (long long)(ja + p.H) * p.ld + PADL + cl;
   const int nin = jb - ja + 2 * K * R;
+  const int nst = (nin + RPS - 1) / RPS;             // ring stages of the segment
   if (c0 + wbase >= p.nx + R) {
     // the whole warp window lies right of the last ghost column (ragged last
     // strip): nothing to compute, keep the TMA ring in step
-    for (int kk = 0; kk < nin; ++kk) {
+    for (int s = 0; s < nst; ++s) {
       mbar_wait_a(ws.full_a + 8u * ws.stage, ws.phase);
       __syncwarp();
       if (lane == 0) mbar_arrive_a(ws.empty_a + 8u * ws.stage);
@@ -232,25 +269,36 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
     }
     return;
   }
-  int k0 = 0;
-  for (; k0 + P <= nin; k0 += P) {                  // full periods: no guards
-#pragma unroll
-    for (int ph = 0; ph < P; ++ph)
-      warp_step<STENCIL, NW, K, C, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s,
-                                                        acc_m);
+  // U stages make a whole number of register-ring periods (U RPS = 0 mod P),
+  // so the ring slot of every row is compile-time inside a period
+  constexpr int U = (RPS % P == 0) ? 1 : P;
+  constexpr int UR = U * RPS;
+  int s0 = 0;
+  for (; (s0 + U) * RPS <= nin; s0 += U) {          // full periods: no guards
+#define CJM_V4_STAGE(u)                                                                   \
+  if (u < U)                                                                              \
+    warp_stage<STENCIL, NW, K, C, RPS, ((u < U ? u : 0) * RPS) % P, false, REDUCE, STORE, \
+               FAST>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin, lane, acc_s, acc_m);
+    CJM_V4_STAGE(0) CJM_V4_STAGE(1) CJM_V4_STAGE(2) CJM_V4_STAGE(3) CJM_V4_STAGE(4)
+#undef CJM_V4_STAGE
   }
-#pragma unroll
-  for (int ph = 0; ph < P - 1; ++ph)                 // tail
-    if (k0 + ph < nin)
-      warp_step<STENCIL, NW, K, C, REDUCE, STORE, FAST>(ws, ls, p, su, sg, k0 + ph, ph, lane, acc_s,
-                                                        acc_m);
-  // the last R(K-1) slots of the segment were still held: release them
-  if (K > 1) {
+  static_assert(U <= 5, "stages per period <= 5");
+  // tail: fewer than UR rows left, in at most U stages (rows >= nin guarded)
+#define CJM_V4_TAIL(u)                                                                     \
+  if (u < U && s0 + u < nst)                                                               \
+    warp_stage<STENCIL, NW, K, C, RPS, ((u < U ? u : 0) * RPS) % P, true, REDUCE, STORE,   \
+               FAST>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin, lane, acc_s, acc_m);
+  CJM_V4_TAIL(0) CJM_V4_TAIL(1) CJM_V4_TAIL(2) CJM_V4_TAIL(3) CJM_V4_TAIL(4)
+#undef CJM_V4_TAIL
+  (void)UR;
+  // the last HS stages of the segment were still held: release them
+  constexpr int HS = ((K - 1) * R + RPS - 1) / RPS;
+  if (HS > 0) {
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
 #pragma unroll
-      for (int i = (K - 1) * R; i > 0; --i) {
+      for (int i = HS; i > 0; --i) {
         int rel = ws.stage - i;
         if (rel < 0) rel += p.stages;
         mbar_arrive_a(ws.empty_a + 8u * rel);
@@ -259,14 +307,21 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
   }
 }
 
-// K = 2 is register-limited to 2 CTAs (10 warps) per SM at its natural 168
-// registers; asking for 3 resident CTAs caps it at 136 (V4_MIN_BLOCKS_K2).
-#ifndef V4_MIN_BLOCKS_K2
-#define V4_MIN_BLOCKS_K2 1
-#endif
-template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE>
-__global__ void __launch_bounds__(32 * NW + 32, (K == 2 && C == 4 ? V4_MIN_BLOCKS_K2 : 1))
-cjm_sweep_kernel_v4(const SweepParams p) {
+// Register cap.  The register file is split between the 4 SM sub-partitions
+// (16 K registers each), so 2 resident CTAs of 5 warps (3 warps on some
+// sub-partition) need <= 168 registers per thread: 172 registers (one more
+// live value) silently halve the occupancy of the K = 2 kernel (58 vs 38 us
+// per sweep at 4096^2, ncu occupancy_limit_registers = 1).  Kernels whose
+// natural count is far above 168 (4 columns per lane with K >= 3, the
+// 17-point) keep one CTA per SM and are not capped.
+template <int STENCIL, int K, int C>
+struct V4Regs {
+  static constexpr int value =
+      Point<STENCIL>::R == 1 ? ((C == 2 || K <= 2) ? 168 : 255) : ((C == 2 && K == 1) ? 168 : 255);
+};
+
+template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE, int RPS = 1>
+__global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(const SweepParams p) {
   constexpr int R = Point<STENCIL>::R;
   using WG = WarpGeom<R, K, C>;
   using TG_ = TileV4<R, K, NW, C>;
@@ -274,9 +329,9 @@ cjm_sweep_kernel_v4(const SweepParams p) {
   constexpr int NT = 32 * NW;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* su = reinterpret_cast<double*>(smem_raw);
-  double* sg = su + (size_t)p.stages * TG_::ROW;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sg + (size_t)p.stages * TG_::GROW);
+  double* su = reinterpret_cast<double*>(smem_raw);            // stages x RPS u rows
+  double* sg = su + (size_t)p.stages * RPS * TG_::ROW;          // stages x RPS g rows
+  uint64_t* full = reinterpret_cast<uint64_t*>(sg + (size_t)p.stages * RPS * TG_::GROW);
   uint64_t* empty = full + p.stages;
   __shared__ double red_s[NW], red_m[NW];
   __shared__ int is_last;
@@ -325,19 +380,34 @@ cjm_sweep_kernel_v4(const SweepParams p) {
         const int gcols = min(c0 + TG_::TG, p.nx) - gc0;
         const uint32_t gbytes = gcols > 0 ? (uint32_t)(((gcols + 1) & ~1) * 8) : 0u;
         const int nin = jb - ja + 2 * K * R;
-        for (int k = 0; k < nin; ++k) {
+        for (int k0 = 0; k0 < nin; k0 += RPS) {       // one ring stage: rows k0 .. k0+RPS-1
           if (used >= p.stages) mbar_wait_a(empty_a + 8u * stage, phase ^ 1u);
-          const int gin = ja - K * R + k;
-          const bool hasu = gin >= -p.H && gin < rows + p.H;
-          const int g1 = gin - R;
-          const bool hasg = k >= 2 * R && g1 >= p.row_lo && g1 < p.row_hi && gbytes;
-          mbar_arrive_expect_tx(&full[stage], (hasu ? ubytes : 0u) + (hasg ? gbytes : 0u));
-          if (hasu)
-            tma_row_load(su + (size_t)stage * TG_::ROW,
-                         src + (long long)(gin + p.H) * ld + (PADL - 2) + c0, ubytes, &full[stage], pol);
-          if (hasg)
-            tma_row_load(sg + (size_t)stage * TG_::GROW + (gc0 - c0),
-                         p.g + (long long)(g1 + p.H) * ld + PADL + gc0, gbytes, &full[stage], pol);
+          uint32_t tx = 0;
+#pragma unroll
+          for (int r = 0; r < RPS; ++r) {
+            const int k = k0 + r;
+            const int gin = ja - K * R + k;
+            const int g1 = gin - R;
+            const bool hasu = k < nin && gin >= -p.H && gin < rows + p.H;
+            const bool hasg = k < nin && k >= 2 * R && g1 >= p.row_lo && g1 < p.row_hi && gbytes;
+            tx += (hasu ? ubytes : 0u) + (hasg ? gbytes : 0u);
+          }
+          mbar_arrive_expect_tx(&full[stage], tx);
+#pragma unroll
+          for (int r = 0; r < RPS; ++r) {
+            const int k = k0 + r;
+            const int gin = ja - K * R + k;
+            const int g1 = gin - R;
+            const bool hasu = k < nin && gin >= -p.H && gin < rows + p.H;
+            const bool hasg = k < nin && k >= 2 * R && g1 >= p.row_lo && g1 < p.row_hi && gbytes;
+            if (hasu)
+              tma_row_load(su + ((size_t)stage * RPS + r) * TG_::ROW,
+                           src + (long long)(gin + p.H) * ld + (PADL - 2) + c0, ubytes, &full[stage],
+                           pol);
+            if (hasg)
+              tma_row_load(sg + ((size_t)stage * RPS + r) * TG_::GROW + (gc0 - c0),
+                           p.g + (long long)(g1 + p.H) * ld + PADL + gc0, gbytes, &full[stage], pol);
+          }
           ++used;
           if (++stage == p.stages) { stage = 0; phase ^= 1u; }
         }
@@ -371,11 +441,11 @@ cjm_sweep_kernel_v4(const SweepParams p) {
       const bool fast = ja - K * R >= p.row_lo && jb + K * R <= p.row_hi && cw >= 0 &&
                         cw + WG::WSPAN <= p.nx;
       if (fast)
-        warp_segment<STENCIL, NW, K, C, REDUCE, STORE, true>(ws, p, su, sg, dst, ja, jb, c0, warp,
-                                                             lane, acc_s, acc_m);
+        warp_segment<STENCIL, NW, K, C, RPS, REDUCE, STORE, true>(ws, p, su, sg, dst, ja, jb, c0,
+                                                                  warp, lane, acc_s, acc_m);
       else
-        warp_segment<STENCIL, NW, K, C, REDUCE, STORE, false>(ws, p, su, sg, dst, ja, jb, c0, warp,
-                                                              lane, acc_s, acc_m);
+        warp_segment<STENCIL, NW, K, C, RPS, REDUCE, STORE, false>(ws, p, su, sg, dst, ja, jb, c0,
+                                                                   warp, lane, acc_s, acc_m);
       uu = seg_end;
     }
   }

@@ -45,14 +45,16 @@ if __name__ == "__main__":
     ap.add_argument("--ks", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
     ap.add_argument("--variants", type=lambda v: [int(x) for x in v.split(",")], default=[3, 4])
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--stages-list", type=lambda v: [int(x) for x in v.split(",")], default=[4, 8, 12])
+    ap.add_argument("--cps-list", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
     a = ap.parse_args()
     if a.tune:
         for cfgname in a.config.split(","):
             grid = []
             for var in a.variants:
                 tws = (256, 512) if var == 3 else (256,)
-                grid += [(var, K, tw, stg, cps) for K in a.ks for tw in tws for stg in (4, 8, 12)
-                         for cps in (1, 2, 3, 4)]
+                grid += [(var, K, tw, stg, cps) for K in a.ks for tw in tws for stg in a.stages_list
+                         for cps in a.cps_list]
             for var, K, tw, stg, cps in grid:
                 try:
                     print(json.dumps(run(cfgname, 2400, 240, variant=var, tile_w=tw, stages=stg,

@@ -56,11 +56,11 @@ SHAPES = [(8, 8), (64, 64), (100, 37), (257, 300), (513, 70), (1000, 11), (4, 4)
 
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("nx,ny", SHAPES)
-@pytest.mark.parametrize("tile_w,variant", [(256, 3), (512, 3), (0, 4), (0, 5)])
+@pytest.mark.parametrize("tile_w,variant", [(256, 3), (512, 3), (0, 4), (0, 5), (0, 6), (0, 7)])
 def test_one_sweep_bitwise(stencil, nx, ny, tile_w, variant):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=inputs.SEED_BASE + nx + 7 * ny)
-    kw = dict(temporal_k=1) if (stencil == 17 and variant in (4, 5)) else {}
+    kw = dict(temporal_k=1) if (stencil == 17 and variant >= 4) else {}
     with cjm.Plan(stencil, nx, ny, h, 1e-8, tile_w=tile_w, variant=variant, **kw) as plan:
         w = plan.info()["weights"]
         g = oracle.rhs_to_g(stencil, h, b)
@@ -76,12 +76,12 @@ def test_one_sweep_bitwise(stencil, nx, ny, tile_w, variant):
 @pytest.mark.parametrize("nx,ny,count", [(300, 257, 37), (1030, 515, 20), (64, 64, 324),
                                          (9, 700, 13), (520, 6, 11)])
 @pytest.mark.parametrize("temporal_k", (1, 2, 3, 4))
-@pytest.mark.parametrize("variant", (3, 4, 5))
+@pytest.mark.parametrize("variant", (3, 4, 5, 6, 7))
 def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
     """A run of sweeps through the CUDA-graph hot loop (spans several graph
     chunks when count > graph_chunk), K sweeps fused per launch (temporal
     blocking), every kernel variant, vs the oracle sweep by sweep."""
-    if stencil == 17 and ((variant == 4 and temporal_k > 1) or (variant == 5 and temporal_k > 2)):
+    if stencil == 17 and ((variant in (4, 6) and temporal_k > 1) or (variant in (5, 7) and temporal_k > 2)):
         pytest.skip("17-point warp-tiled kernels: K=1 (4 columns/lane) or K<=2 (2 columns/lane)")
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=3)
@@ -105,7 +105,11 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
                                  dict(variant=4, temporal_k=3, stages=8, ctas_per_sm=1),
                                  dict(variant=4, temporal_k=1, stages=2),
                                  dict(variant=5, temporal_k=2, stages=6, ctas_per_sm=3),
-                                 dict(variant=5, temporal_k=4, stages=8)])
+                                 dict(variant=5, temporal_k=4, stages=8),
+                                 dict(variant=6, temporal_k=2, stages=3, ctas_per_sm=1),
+                                 dict(variant=6, temporal_k=4, stages=5),
+                                 dict(variant=7, temporal_k=3, stages=3),
+                                 dict(variant=7, temporal_k=1, stages=8, ctas_per_sm=3)])
 def test_launch_configuration_does_not_change_result(cfg):
     nx, ny = 777, 301
     u0, b, h = inputs.test_problem(nx, ny, 1, init="random", seed=5)
@@ -135,13 +139,14 @@ def test_residual_matches_oracle(stencil):  # noqa: D103
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("n,init", [(64, "zero"), (64, "random"), (200, "zero"), (129, "random")])
 @pytest.mark.parametrize("temporal_k,variant,resident", [(1, 4, -1), (2, 4, -1), (2, 3, -1), (4, 3, -1),
-                                                          (3, 0, -1), (0, 0, 1), (2, 5, -1)])
+                                                          (3, 0, -1), (0, 0, 1), (2, 5, -1), (2, 6, -1),
+                                                          (3, 7, -1)])
 def test_solve_matches_oracle(stencil, n, init, temporal_k, variant, resident):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(n, n, r, init=init)
     uo, ro = oracle.solve(stencil, h, 1e-8, b, u0)
-    if stencil == 17 and variant in (4, 5) and temporal_k > 1:
-        variant = 0 if variant == 4 else variant
+    if stencil == 17 and variant >= 4 and temporal_k > 1:
+        variant = {4: 0, 5: 5, 6: 0, 7: 7}[variant] if temporal_k <= 2 else 0
     with cjm.Plan(stencil, n, n, h, 1e-8, temporal_k=temporal_k, variant=variant,
                   resident=resident) as plan:
         assert plan.info()["resident"] == (1 if resident == 1 else 0)

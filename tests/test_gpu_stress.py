@@ -21,7 +21,7 @@ from paper_1705_00103_b200 import cjm  # noqa: E402
 
 
 @pytest.mark.parametrize("variant,K,stages", [(4, 1, 2), (4, 2, 3), (4, 3, 4), (3, 1, 2), (4, 1, 4),
-                                              (5, 2, 3)])
+                                              (5, 2, 3), (6, 1, 2), (6, 2, 3), (7, 3, 3)])
 def test_ring_reuse_is_race_free(variant, K, stages):
     n, cnt, trials = 1024, 16, 60
     u0, b, h = inputs.test_problem(n, n, 1, init="random")
