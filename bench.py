@@ -331,7 +331,12 @@ def main():
                          "sweeps_per_launch": K,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "avg_launch_us": 1e6 * t_launch,
-                         "sweep_glups": K * float(nx) * nyl / t_launch / 1e9},
+                         "sweep_glups": K * float(nx) * nyl / t_launch / 1e9,
+                         # the same launches against the single-sweep roofline
+                         # (24 B per lattice update): > 1 because a
+                         # launch moves 24 B per node for K updates
+                         "lup_roofline_frac": K * float(nx) * nyl / t_launch * BYTES_PER_LUP
+                                              / 1e9 / peak},
             "breakdown_ms": {"plan": 1e3 * statistics.mean(r["plan_s"] for r in reps),
                              "solve_device": 1e3 * statistics.mean(r["solve_s"] for r in reps),
                              "hot_sweeps": 1e3 * statistics.mean(r["sweep_s"] for r in reps)},

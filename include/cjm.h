@@ -125,6 +125,9 @@ typedef struct {
     int band_split;        /* 1: run every K=1 hot sweep as boundary-band launches +
                               interior launch (the multi-GPU overlap schedule) even
                               without NCCL; for tests */
+    int warps;             /* variant 7 only: consumer warps per CTA, 4, 5 or 7
+                              (0 = the count that keeps the most consumer warps
+                              resident per SM) */
 } cjm_options;
 
 typedef struct {
@@ -148,6 +151,9 @@ typedef struct {
     int rhs_ghost_rows;        /* extra rows above / below the slab in the caller's rhs */
     double h2d_bytes, d2h_bytes;  /* host<->device bytes moved by the call */
     double real_error;     /* cjm_solve_ref: max |u - u_ref| of the returned iterate */
+    int variant, warps, stages, ctas;  /* launch configuration of the plan's sweep kernel:
+                                          variant, consumer warps per CTA, TMA ring
+                                          stages, persistent CTAs */
 } cjm_report;
 
 typedef struct cjm_plan_s *cjm_plan_t;

@@ -54,7 +54,7 @@ class Options(C.Structure):
                 ("temporal_k", C.c_int), ("variant", C.c_int),
                 ("tile_w", C.c_int),
                 ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int),
-                ("resident", C.c_int), ("band_split", C.c_int)]
+                ("resident", C.c_int), ("band_split", C.c_int), ("warps", C.c_int)]
 
 
 class HaloMsg(C.Structure):
@@ -71,7 +71,8 @@ class Report(C.Structure):
                 ("sweeps_timed", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("hot_launches", C.c_longlong), ("temporal_k", C.c_int), ("resident", C.c_int),
                 ("ghost_rows", C.c_int), ("rhs_ghost_rows", C.c_int),
-                ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("real_error", C.c_double)]
+                ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("real_error", C.c_double),
+                ("variant", C.c_int), ("warps", C.c_int), ("stages", C.c_int), ("ctas", C.c_int)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -117,50 +117,53 @@ KernelFn pick_nt(int NT, int K, int mode) {
 
 // warp-tiled variant (sweep_v4.cuh), 4 consumer warps, C columns per lane,
 // RPS input rows per TMA ring stage
-template <int ST, int K, int C, int RPS>
+template <int ST, int K, int C, int RPS, int NW = 4>
 KernelFn pick_mode_v4(int mode) {
   switch (mode) {
-    case MODE_HOT: return cjm::cjm_sweep_kernel_v4<ST, 4, K, C, false, true, RPS>;
-    case MODE_CHECK: return cjm::cjm_sweep_kernel_v4<ST, 4, K, C, true, true, RPS>;
-    default: return cjm::cjm_sweep_kernel_v4<ST, 4, 1, C, true, false, RPS>;
+    case MODE_HOT: return cjm::cjm_sweep_kernel_v4<ST, NW, K, C, false, true, RPS>;
+    case MODE_CHECK: return cjm::cjm_sweep_kernel_v4<ST, NW, K, C, true, true, RPS>;
+    default: return cjm::cjm_sweep_kernel_v4<ST, NW, 1, C, true, false, RPS>;
   }
 }
 
 // the 17-point warp-tiled kernel with K >= 2 does not fit the register file
 // (5-row rings of 4 columns x 3 arrays per level): not instantiated, the plan
 // uses the shared-line variant there
-template <int ST, int C, int RPS>
+template <int ST, int C, int RPS, int NW = 4>
 KernelFn pick_k_v4(int K, int mode) {
   if constexpr (ST == 17 && C == 4) {
-    return K == 1 ? pick_mode_v4<ST, 1, C, RPS>(mode) : nullptr;
+    return K == 1 ? pick_mode_v4<ST, 1, C, RPS, NW>(mode) : nullptr;
   } else if constexpr (ST == 17) {
-    return K == 1 ? pick_mode_v4<ST, 1, C, RPS>(mode)
-                  : K == 2 ? pick_mode_v4<ST, 2, C, RPS>(mode) : nullptr;
+    return K == 1 ? pick_mode_v4<ST, 1, C, RPS, NW>(mode)
+                  : K == 2 ? pick_mode_v4<ST, 2, C, RPS, NW>(mode) : nullptr;
   } else {
     switch (K) {
-      case 1: return pick_mode_v4<ST, 1, C, RPS>(mode);
-      case 2: return pick_mode_v4<ST, 2, C, RPS>(mode);
-      case 3: return pick_mode_v4<ST, 3, C, RPS>(mode);
-      default: return pick_mode_v4<ST, 4, C, RPS>(mode);
+      case 1: return pick_mode_v4<ST, 1, C, RPS, NW>(mode);
+      case 2: return pick_mode_v4<ST, 2, C, RPS, NW>(mode);
+      case 3: return pick_mode_v4<ST, 3, C, RPS, NW>(mode);
+      default: return pick_mode_v4<ST, 4, C, RPS, NW>(mode);
     }
   }
 }
 
-template <int C, int MULTI>   // MULTI: 2r+1 rows per ring stage
+template <int C, int MULTI, int NW = 4>   // MULTI: 2r+1 rows per ring stage
 KernelFn pick_st_v4(int stencil, int K, int mode) {
   switch (stencil) {
-    case 5: return pick_k_v4<5, C, MULTI ? 3 : 1>(K, mode);
-    case 9: return pick_k_v4<9, C, MULTI ? 3 : 1>(K, mode);
-    default: return pick_k_v4<17, C, MULTI ? 5 : 1>(K, mode);
+    case 5: return pick_k_v4<5, C, MULTI ? 3 : 1, NW>(K, mode);
+    case 9: return pick_k_v4<9, C, MULTI ? 3 : 1, NW>(K, mode);
+    default: return pick_k_v4<17, C, MULTI ? 5 : 1, NW>(K, mode);
   }
 }
 
-KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode) {
+// nw: consumer warps per CTA (variant 7 only: 4, 5 or 7)
+KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode, int nw = 4) {
   switch (variant) {      // warp-tiled: 4 / 2 columns per lane, 1 / 2r+1 rows per stage
     case 4: return pick_st_v4<4, 0>(stencil, K, mode);
     case 5: return pick_st_v4<2, 0>(stencil, K, mode);
     case 6: return pick_st_v4<4, 1>(stencil, K, mode);
-    case 7: return pick_st_v4<2, 1>(stencil, K, mode);
+    case 7:
+      return nw == 5 ? pick_st_v4<2, 1, 5>(stencil, K, mode)
+           : nw == 7 ? pick_st_v4<2, 1, 7>(stencil, K, mode) : pick_st_v4<2, 1, 4>(stencil, K, mode);
     default: break;
   }
   switch (stencil) {
@@ -233,7 +236,8 @@ struct cjm_plan_s {
   size_t small_bytes = 0;
   // launch configuration
   int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
-  int variant = 4;   // 3: shared-line levels (sweep.cuh), 4: warp-tiled (sweep_v4.cuh)
+  int variant = 4;   // 3: shared-line levels (sweep.cuh), 4-7: warp-tiled (sweep_v4.cuh)
+  int nw = 4;        // consumer warps per CTA (warp-tiled)
   int band_split = 0;  // split hot sweeps into boundary / interior bands even without NCCL
   // resident (whole grid in shared memory) hot path
   int resident = 0, res_ctas = 0, res_rows = 0;
@@ -258,13 +262,13 @@ namespace {
 int v4_cpl(int variant) { return (variant == 5 || variant == 7) ? 2 : 4; }
 int v4_rps(int variant, int R) { return variant >= 6 ? 2 * R + 1 : 1; }   // rows per ring stage
 
-int v4_tout(int R, int K, int C) {      // owned columns per CTA strip, warp-tiled variant
+int v4_tout(int R, int K, int C, int nw) {   // owned columns per CTA strip, warp-tiled variant
   const int E = K == 1 ? 0 : ((R * (K - 1) + 1) & ~1);
-  return 4 * (32 * C - 2 * E);
+  return nw * (32 * C - 2 * E);
 }
 
 int tile_out(const cjm_plan_s* pl, int K) {
-  if (pl->variant >= 4) return v4_tout(pl->R, K, v4_cpl(pl->variant));
+  if (pl->variant >= 4) return v4_tout(pl->R, K, v4_cpl(pl->variant), pl->nw);
   return 2 * pl->NT - 2 * tile_e(pl->R, K);
 }
 
@@ -273,7 +277,7 @@ size_t smem_bytes(const cjm_plan_s* pl, int K) {
     const int C = v4_cpl(pl->variant);
     const int E = K == 1 ? 0 : ((pl->R * (K - 1) + 1) & ~1);
     const int WOUT = 32 * C - 2 * E;
-    const int TG = 3 * WOUT + 32 * C;
+    const int TG = (pl->nw - 1) * WOUT + 32 * C;
     const int ROW = (TG + 4 + 7) / 8 * 8, GROW = (TG + 7) / 8 * 8;
     return (size_t)pl->stages * v4_rps(pl->variant, pl->R) * (ROW + GROW) * sizeof(double) +
            2 * (size_t)pl->stages * sizeof(uint64_t);
@@ -284,7 +288,7 @@ size_t smem_bytes(const cjm_plan_s* pl, int K) {
          2 * (size_t)pl->stages * sizeof(uint64_t);
 }
 
-int block_threads(const cjm_plan_s* pl) { return pl->variant >= 4 ? 4 * 32 + 32 : pl->NT + 32; }
+int block_threads(const cjm_plan_s* pl) { return pl->variant >= 4 ? pl->nw * 32 + 32 : pl->NT + 32; }
 
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur.
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur, over the
@@ -347,7 +351,7 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int ro
   const long long nstrips = (pl->nx + tout - 1) / tout;
   sp.units = nstrips * nrows;
   const int grid = (int)std::min<long long>(pl->nctas, sp.units);
-  KernelFn k = pick_kernel(pl->stencil, pl->variant, pl->NT, K, mode);
+  KernelFn k = pick_kernel(pl->stencil, pl->variant, pl->NT, K, mode, pl->nw);
   k<<<grid, block_threads(pl), smem_bytes(pl, K), st>>>(sp);
   CUDA_TRY(cudaGetLastError());
   pl->launches += 1;
@@ -618,6 +622,10 @@ void fill_static(const cjm_plan_s* pl, cjm_report* r) {
   r->plan_s = pl->plan_s;
   r->temporal_k = pl->K;
   r->resident = pl->resident;
+  r->variant = pl->variant;
+  r->warps = pl->variant >= 4 ? pl->nw : pl->NT / 32;
+  r->stages = pl->stages;
+  r->ctas = pl->nctas;
   r->ghost_rows = pl->Hu;
   r->rhs_ghost_rows = pl->Hr;
 }
@@ -961,17 +969,18 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   // persistent interior kernel
   pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : (opt.world_size > 1 ? 3 : 4);
   // Default: the warp-tiled kernel with 2 columns per lane and 2r+1 rows per
-  // TMA stage (variant 7).  5/9-point: three sweeps per launch, four from
-  // 8192^2 up; 17-point: two (profiles/r01_v7_tune.jsonl: 31.3 us per 9-point
-  // sweep at 4096^2 vs 37.9 for variant 4 at K = 2; 443 vs 599 at 16384^2;
-  // 242 vs 290 per 17-point sweep at 8192^2 for variant 3 at K = 1).  An
-  // explicit tile_w selects the shared-line kernel (variant 3).
+  // TMA stage (variant 7), consumer warps per CTA chosen below.  5/9-point:
+  // four sweeps per launch from 4096^2 up, three below; 17-point: two
+  // (profiles/r01_v7_tune.jsonl: 27.3 us per 9-point sweep at 4096^2 vs 37.9
+  // for variant 4 at K = 2; 404 vs 599 at 16384^2; 167 vs 290 per 17-point
+  // sweep at 8192^2 for variant 3 at K = 1).  An explicit tile_w selects the
+  // shared-line kernel (variant 3).
   const bool wide = stencil == 17;
   pl->NT = opt.tile_w == 512 || (opt.tile_w == 0 && wide) ? 256 : 128;
   pl->variant = opt.variant ? opt.variant : (opt.tile_w ? 3 : 7);
   pl->band_split = opt.band_split;
   pl->K = opt.temporal_k > 0 ? opt.temporal_k
-                             : (wide ? 2 : ((long long)nx * ny >= 8192LL * 8192LL ? 4 : 3));
+                             : (wide ? 2 : ((long long)nx * ny >= 4096LL * 4096LL ? 4 : 3));
   // multi-GPU: K-fused launches need H = K r deep halos, exchanged after every
   // launch; the slab must stay thicker than 2H + 1 rows (else fall back to K=1)
   if (pl->world > 1 && nyl < 2 * pl->K * R + 1) pl->K = 1;
@@ -992,6 +1001,40 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   // resident).  Check / residual / remainder kernels may need more registers;
   // they then run the same grid in more than one wave, which is correct
   // because no CTA ever waits for another.
+  if ((opt.warps != 0 && (pl->variant != 7 || (opt.warps != 4 && opt.warps != 5 && opt.warps != 7))) ||
+      opt.warps < 0) {
+    set_error("cjm_plan", "warps must be 4, 5 or 7, with variant 7");
+    return fail(CJM_ERR_INVALID_ARG);
+  }
+  if (pl->variant == 7) {
+    // Consumer warps per CTA and ring depth: the pair that keeps the most
+    // consumer warps resident per SM (registers are split between the SM's
+    // 4 sub-partitions, shared memory holds stages x (2r+1) rows per CTA);
+    // ties: the deeper ring, then fewer warps.
+    const int nws[3] = {4, 5, 7};
+    const int st_hi = opt.stages > 0 ? opt.stages : (R == 1 ? 6 : 4);
+    const int st_lo = opt.stages > 0 ? opt.stages : 4;
+    int best = -1, best_nw = 4, best_st = st_hi;
+    for (int i = 0; i < 3; ++i) {
+      if (opt.warps && nws[i] != opt.warps) continue;
+      for (int stg = st_hi; stg >= st_lo; --stg) {
+        pl->nw = nws[i];
+        pl->stages = stg;
+        const size_t sm = smem_bytes(pl, pl->K);
+        if (sm > (size_t)smem_optin - 2048) continue;
+        KernelFn k = pick_kernel(stencil, 7, pl->NT, pl->K, MODE_HOT, pl->nw);
+        PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sm));
+        int occ = 0;
+        PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k,
+                                                                block_threads(pl), sm));
+        const int score = std::min(occ, pl->ctas_per_sm) * pl->nw;
+        if (score > best) { best = score; best_nw = pl->nw; best_st = stg; }
+      }
+    }
+    pl->nw = best_nw;
+    pl->stages = best_st;
+  }
   if (pl->variant >= 4 &&
       pl->stages < ((pl->K - 1) * R + v4_rps(pl->variant, R) - 1) / v4_rps(pl->variant, R) + 2) {
     // the warp-tiled kernel holds a stage until level K-1 has read the g rows
@@ -1009,7 +1052,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     if (K != 1 && K != pl->K) continue;
     for (int mode = 0; mode < 3; ++mode) {
       if (mode == MODE_RESID && K != 1) continue;
-      KernelFn k = pick_kernel(stencil, pl->variant, pl->NT, K, mode);
+      KernelFn k = pick_kernel(stencil, pl->variant, pl->NT, K, mode, pl->nw);
       const size_t sm = smem_bytes(pl, K);
       PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sm));

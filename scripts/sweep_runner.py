@@ -28,6 +28,8 @@ def run(config, count, warm, **kw):
         rep = plan.sweeps(bd, ud, 1, count)
     us = 1e6 * rep["sweep_s"] / count
     K = rep["temporal_k"]
+    kw = dict(kw, variant=rep["variant"], warps=rep["warps"], stages=rep["stages"], ctas=rep["ctas"],
+              temporal_k=K)
     return dict(config=config, **kw, us_per_sweep=us, glups=nx * ny / (us * 1e-6) / 1e9,
                 gbs_per_launch=24.0 * nx * ny / (K * us * 1e-6) / 1e9)
 
@@ -45,6 +47,7 @@ if __name__ == "__main__":
     ap.add_argument("--ks", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
     ap.add_argument("--variants", type=lambda v: [int(x) for x in v.split(",")], default=[3, 4])
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--stages-list", type=lambda v: [int(x) for x in v.split(",")], default=[4, 8, 12])
     ap.add_argument("--cps-list", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
     a = ap.parse_args()
@@ -64,4 +67,5 @@ if __name__ == "__main__":
                                           ctas_per_sm=cps, temporal_k=K, error=str(e))), flush=True)
     else:
         print(json.dumps(run(a.config, a.count, a.warm, tile_w=a.tile_w, stages=a.stages,
-                             ctas_per_sm=a.ctas_per_sm, temporal_k=a.temporal_k, variant=a.variant)))
+                             ctas_per_sm=a.ctas_per_sm, temporal_k=a.temporal_k, variant=a.variant,
+                             warps=a.warps)))

@@ -109,7 +109,10 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
                                  dict(variant=6, temporal_k=2, stages=3, ctas_per_sm=1),
                                  dict(variant=6, temporal_k=4, stages=5),
                                  dict(variant=7, temporal_k=3, stages=3),
-                                 dict(variant=7, temporal_k=1, stages=8, ctas_per_sm=3)])
+                                 dict(variant=7, temporal_k=1, stages=8, ctas_per_sm=3),
+                                 dict(variant=7, warps=5, temporal_k=4, stages=6),
+                                 dict(variant=7, warps=7, temporal_k=2, stages=3),
+                                 dict(variant=7, warps=4, temporal_k=3, stages=5, ctas_per_sm=1)])
 def test_launch_configuration_does_not_change_result(cfg):
     nx, ny = 777, 301
     u0, b, h = inputs.test_problem(nx, ny, 1, init="random", seed=5)
