@@ -128,6 +128,11 @@ typedef struct {
     int warps;             /* variant 7 only: consumer warps per CTA, 4, 5 or 7
                               (0 = the count that keeps the most consumer warps
                               resident per SM) */
+    int chunk_rows;        /* warp-tiled variants: rows per work item that the CTAs of a
+                              non-reducing launch take from a device counter (dynamic load
+                              balancing); 0 = automatic (256 / 128 rows when every CTA
+                              gets >= 2048 / 1024 rows, else static), -1 = static
+                              contiguous ranges per CTA */
 } cjm_options;
 
 typedef struct {

@@ -54,7 +54,8 @@ class Options(C.Structure):
                 ("temporal_k", C.c_int), ("variant", C.c_int),
                 ("tile_w", C.c_int),
                 ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int),
-                ("resident", C.c_int), ("band_split", C.c_int), ("warps", C.c_int)]
+                ("resident", C.c_int), ("band_split", C.c_int), ("warps", C.c_int),
+                ("chunk_rows", C.c_int)]
 
 
 class HaloMsg(C.Structure):

@@ -157,6 +157,16 @@ KernelFn pick_st_v4(int stencil, int K, int mode) {
 
 // nw: consumer warps per CTA (variant 7 only: 4, 5 or 7)
 KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode, int nw = 4) {
+#ifdef CJM_EXPERIMENT_9PT_V7
+  // measurement builds (build.build(defines=..., out=...)): only the 9-point
+  // variant-7 kernels, so an experiment compiles in seconds
+  if (stencil != 9 || variant != 7) return nullptr;
+  switch (nw) {
+    case 5: return pick_k_v4<9, 2, 3, 5>(K, mode);
+    case 7: return pick_k_v4<9, 2, 3, 7>(K, mode);
+    default: return pick_k_v4<9, 2, 3, 4>(K, mode);
+  }
+#else
   switch (variant) {      // warp-tiled: 4 / 2 columns per lane, 1 / 2r+1 rows per stage
     case 4: return pick_st_v4<4, 0>(stencil, K, mode);
     case 5: return pick_st_v4<2, 0>(stencil, K, mode);
@@ -171,6 +181,7 @@ KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode, int nw =
     case 9: return pick_nt<9>(NT, K, mode);
     default: return pick_nt<17>(NT, K, mode);
   }
+#endif
 }
 
 // halo columns lost per side by K-1 on-chip levels (mirror of TileGeom::E)
@@ -180,6 +191,7 @@ __global__ void set_state_kernel(cjm::SweepState* st, unsigned long long n) {
   st->n = n;
   st->cur = 0u;
   st->ticket = 0u;
+  st->next_chunk = 0u;
 }
 
 }  // namespace
@@ -238,6 +250,8 @@ struct cjm_plan_s {
   int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
   int variant = 4;   // 3: shared-line levels (sweep.cuh), 4-7: warp-tiled (sweep_v4.cuh)
   int nw = 4;        // consumer warps per CTA (warp-tiled)
+  int chunk_rows = -1;  // warp-tiled hot launches: rows per dynamically scheduled work item
+                        // (0: static ranges, -1: chosen per launch)
   int band_split = 0;  // split hot sweeps into boundary / interior bands even without NCCL
   // resident (whole grid in shared memory) hot path
   int resident = 0, res_ctas = 0, res_rows = 0;
@@ -351,6 +365,18 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int ro
   const long long nstrips = (pl->nx + tout - 1) / tout;
   sp.units = nstrips * nrows;
   const int grid = (int)std::min<long long>(pl->nctas, sp.units);
+  // Dynamic balancing for hot launches of the warp-tiled kernels only (a
+  // reducing launch keeps static per-CTA ranges: bitwise-reproducible sums).
+  // Auto: only when every CTA gets >= ~8 work items, since each item re-reads
+  // and recomputes 2 K r halo rows (measured, profiles/r01_v7_chunks.jsonl:
+  // 16384^2 K=4 330 vs 415 us per sweep with 256-row items; 4096^2, 208 rows
+  // per CTA, is faster static).
+  int chunk = 0;
+  if (mode == MODE_HOT && pl->variant >= 4) {
+    const long long per_cta = sp.units / std::max(grid, 1);
+    chunk = pl->chunk_rows >= 0 ? pl->chunk_rows : per_cta >= 2048 ? 256 : per_cta >= 1024 ? 128 : 0;
+  }
+  sp.chunk_rows = chunk;
   KernelFn k = pick_kernel(pl->stencil, pl->variant, pl->NT, K, mode, pl->nw);
   k<<<grid, block_threads(pl), smem_bytes(pl, K), st>>>(sp);
   CUDA_TRY(cudaGetLastError());
@@ -951,6 +977,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     pl->K = 1;
     pl->NT = cjm::MASK_NT;
     pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
+  pl->chunk_rows = opt.chunk_rows > 0 ? opt.chunk_rows : (opt.chunk_rows < 0 ? 0 : -1);   // -1: auto
     pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 8;
     int occ = 0;
     PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -997,6 +1024,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
                               : (pl->variant >= 6 ? (R == 1 ? 6 : 4)
                                                   : pl->variant >= 4 ? 8 : (pl->NT == 256 ? 12 : 4));
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
+  pl->chunk_rows = opt.chunk_rows > 0 ? opt.chunk_rows : (opt.chunk_rows < 0 ? 0 : -1);   // -1: auto
   // The grid is sized for the hot kernel (persistent: ctas_per_sm per SM, all
   // resident).  Check / residual / remainder kernels may need more registers;
   // they then run the same grid in more than one wave, which is correct
@@ -1345,6 +1373,17 @@ const char* cjm_status_str(int s) {
 }
 
 const char* cjm_last_error(void) { return g_last_error.c_str(); }
+
+#ifdef CJM_DIAG_TIMES
+// diagnostic builds only: the per-CTA (start, end) %globaltimer stamps of the
+// last hot launch, kept in the (otherwise unused) partials of hot launches
+cjm_status cjm_diag_times(cjm_plan_t p, unsigned long long* host, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, p->partials, sizeof(unsigned long long) * 2 * std::min(n, p->nctas),
+             cudaMemcpyDeviceToHost);
+  return (cjm_status)p->nctas;
+}
+#endif
 
 cjm_status cjm_pool_trim(long long* cached_bytes_before) {
   if (cached_bytes_before) *cached_bytes_before = (long long)cjm::pool_cached_bytes();

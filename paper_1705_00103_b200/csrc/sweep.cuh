@@ -46,6 +46,8 @@ struct SweepState {
   unsigned long long n;        // global sweep index of the input iterate
   unsigned int cur;            // buffer holding the input iterate
   unsigned int ticket;         // CTA completion counter (0 between launches)
+  unsigned int next_chunk;     // dynamic work counter of the warp-tiled kernel (0 between launches)
+  unsigned int pad_;
 };
 
 struct SweepParams {
@@ -66,6 +68,9 @@ struct SweepParams {
   int row0, nrows;             // the band of output rows of this launch
   int stages;                  // TMA ring depth
   int advance;                 // the last CTA advances n / flips cur (last launch of a sweep)
+  int chunk_rows;              // warp-tiled kernel: > 0 = CTAs take (strip, chunk_rows rows)
+                               // work items from a device counter (dynamic balancing);
+                               // 0 = one contiguous range of (strip, row) units per CTA
 };
 
 // ---------------------------------------------------------------- PTX helpers

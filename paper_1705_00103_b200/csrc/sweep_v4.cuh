@@ -18,7 +18,14 @@
 //    release per RPS rows, and the RPS rows of a stage are independent
 //    dependency chains at every level, which the compiler interleaves (the
 //    kernel is latency-bound: few warps per SM, long fp64 chains per row).
-// Everything else (pass-through ghosts, the FAST instantiation, the fixed
+//  * work distribution: the producer warp decides the CTA's segments (a column
+//    strip and a row range) and hands each one to the consumer warps in a
+//    per-stage descriptor guarded by the stage's full barrier.  Hot launches
+//    take chunk_rows-row segments from a device counter (CTAs on slower SMs
+//    or with boundary work simply take fewer); launches that reduce keep one
+//    static contiguous range per CTA so that the per-CTA partial sums, and
+//    the residual, are bitwise reproducible.
+// Everything else (pass-through ghosts, the FAST instantiations, the fixed
 // association of DESIGN R6, device-side n / cur, ticket, fixed-order
 // reduction) is as in sweep.cuh.
 #pragma once
@@ -88,8 +95,11 @@ struct LaneSeg {
 // (unconditionally: a level computes garbage until its window is full, which
 // is never stored), store the last level when it is active.  RI and PH are
 // compile-time, so every register-ring slot and every stage offset folds.
+// FM (fast mode): 2 = the warp window holds no ghost / padding column and the
+// segment no ghost row (no checks); 1 = no ghost column, ghost rows possible
+// (one uniform row test per level); 0 = every node checked.
 template <int STENCIL, int NW, int K, int C, int RPS, int RI, int PH, bool REDUCE, bool STORE,
-          bool FAST>
+          int FM>
 __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
                                          const SweepParams& p, const double* su, const double* sg,
                                          int st, int kk, int lane, double& acc_s, double& acc_m) {
@@ -158,7 +168,8 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
       }
       const double J = Point<STENCIL>::jacobi_target(uw, x1, x2, g[j]);
       dd[j] = __dsub_rn(J, uw[R]);
-      o[j] = (FAST || (rowin && ls.in[j])) ? __fma_rn(ws.wl[l], dd[j], uw[R]) : uw[R];
+      o[j] = (FM == 2 || ((FM == 1 || ls.in[j]) && rowin)) ? __fma_rn(ws.wl[l], dd[j], uw[R])
+                                                            : uw[R];
     }
     const bool active = kk >= 2 * (l + 1) * R;
     if (REDUCE && l == 0 && active && (unsigned)(G - ls.ja) < (unsigned)(ls.jb - ls.ja)) {
@@ -185,10 +196,10 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
           // (E even: both columns of a pair are owned or neither).  (Stores
           // predicated inside inline PTX instead of branches measured slower:
           // 32.2 vs 31.4 us per sweep, profiles/r01_v7_tune.jsonl.)
-          const bool ownp = FAST ? (C * lane + j >= E && C * lane + j + 2 <= WG::WSPAN - E)
-                                 : (ls.own[j] && ls.own[j + 1]);
+          const bool ownp = FM >= 1 ? (C * lane + j >= E && C * lane + j + 2 <= WG::WSPAN - E)
+                                    : (ls.own[j] && ls.own[j + 1]);
           if (ownp) *reinterpret_cast<double2*>(ls.outp + j) = make_double2(o[j], o[j + 1]);
-          else if (!FAST) {
+          else if (FM == 0) {
             if (ls.own[j]) ls.outp[j] = o[j];
             if (ls.own[j + 1]) ls.outp[j + 1] = o[j + 1];
           }
@@ -204,7 +215,7 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
 // last stage, when GUARD), then release the stage whose rows level K-1 has
 // now read for the last time.
 template <int STENCIL, int NW, int K, int C, int RPS, int PH0, bool GUARD, bool REDUCE,
-          bool STORE, bool FAST>
+          bool STORE, int FM>
 __device__ __forceinline__ void warp_stage(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
                                            const SweepParams& p, const double* su,
                                            const double* sg, int s, int kk0, int nin, int lane,
@@ -213,11 +224,13 @@ __device__ __forceinline__ void warp_stage(WarpState<Point<STENCIL>::R, K, C>& w
   constexpr int P = 2 * R + 1;
   constexpr int HS = ((K - 1) * R + RPS - 1) / RPS;   // stages held after processing
   const int st = ws.stage;
+#ifndef CJM_DIAG_NOWAIT   // diagnostic builds only: consumers do not wait for their data
   mbar_wait_a(ws.full_a + 8u * st, ws.phase);
+#endif
   if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
 #define CJM_V4_ROW(RI)                                                                         \
   if (RI < RPS && (!GUARD || kk0 + RI < nin))                                                  \
-    warp_row<STENCIL, NW, K, C, RPS, (RI < RPS ? RI : 0), (PH0 + RI) % P, REDUCE, STORE, FAST>( \
+    warp_row<STENCIL, NW, K, C, RPS, (RI < RPS ? RI : 0), (PH0 + RI) % P, REDUCE, STORE, FM>(   \
         ws, ls, p, su, sg, st, kk0 + RI, lane, acc_s, acc_m);
   CJM_V4_ROW(0) CJM_V4_ROW(1) CJM_V4_ROW(2) CJM_V4_ROW(3) CJM_V4_ROW(4)
 #undef CJM_V4_ROW
@@ -232,7 +245,7 @@ __device__ __forceinline__ void warp_stage(WarpState<Point<STENCIL>::R, K, C>& w
   }
 }
 
-template <int STENCIL, int NW, int K, int C, int RPS, bool REDUCE, bool STORE, bool FAST>
+template <int STENCIL, int NW, int K, int C, int RPS, bool REDUCE, bool STORE, int FM>
 __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>& ws,
                                              const SweepParams& p, const double* su,
                                              const double* sg, double* dst, int ja, int jb,
@@ -278,7 +291,7 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
 #define CJM_V4_STAGE(u)                                                                   \
   if (u < U)                                                                              \
     warp_stage<STENCIL, NW, K, C, RPS, ((u < U ? u : 0) * RPS) % P, false, REDUCE, STORE, \
-               FAST>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin, lane, acc_s, acc_m);
+               FM>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin, lane, acc_s, acc_m);
     CJM_V4_STAGE(0) CJM_V4_STAGE(1) CJM_V4_STAGE(2) CJM_V4_STAGE(3) CJM_V4_STAGE(4)
 #undef CJM_V4_STAGE
   }
@@ -287,7 +300,7 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
 #define CJM_V4_TAIL(u)                                                                     \
   if (u < U && s0 + u < nst)                                                               \
     warp_stage<STENCIL, NW, K, C, RPS, ((u < U ? u : 0) * RPS) % P, true, REDUCE, STORE,   \
-               FAST>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin, lane, acc_s, acc_m);
+               FM>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin, lane, acc_s, acc_m);
   CJM_V4_TAIL(0) CJM_V4_TAIL(1) CJM_V4_TAIL(2) CJM_V4_TAIL(3) CJM_V4_TAIL(4)
 #undef CJM_V4_TAIL
   (void)UR;
@@ -335,10 +348,15 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
   uint64_t* empty = full + p.stages;
   __shared__ double red_s[NW], red_m[NW];
   __shared__ int is_last;
+  __shared__ int4 seg_desc[32];   // per ring stage: (strip, ja, jb, valid) of a segment's first stage
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
+#ifdef CJM_DIAG_TIMES
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
 
   if (tid == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -368,11 +386,38 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
       uint32_t phase = 0;
       long long used = 0;
       const uint32_t full_a = smem_addr(full), empty_a = smem_addr(empty);
-      for (long long uu = u_begin; uu < u_end;) {
-        const int strip = (int)(uu / p.nrows);
-        const int ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
-        const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
-        const int jb = ja + (int)(seg_end - uu);
+      const int cpr = p.chunk_rows > 0 ? (p.nrows + p.chunk_rows - 1) / p.chunk_rows : 1;
+      const long long nchunks = (p.units / p.nrows) * cpr;
+      long long uu = u_begin;
+      for (;;) {
+        // ---- next segment: (strip, rows [ja, jb)), or the end marker
+        int strip = 0, ja = 0, jb = 0;
+        bool more;
+        if (p.chunk_rows > 0) {
+          const long long c = atomicAdd(&p.state->next_chunk, 1u);
+          more = c < nchunks;
+          if (more) {
+            strip = (int)(c / cpr);
+            const int q = (int)(c - (long long)strip * cpr);
+            ja = p.row0 + q * p.chunk_rows;
+            jb = min(ja + p.chunk_rows, p.row0 + p.nrows);
+          }
+        } else {
+          more = uu < u_end;
+          if (more) {
+            strip = (int)(uu / p.nrows);
+            ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
+            const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
+            jb = ja + (int)(seg_end - uu);
+            uu = seg_end;
+          }
+        }
+        if (!more) {   // end marker: a stage without data
+          if (used >= p.stages) mbar_wait_a(empty_a + 8u * stage, phase ^ 1u);
+          seg_desc[stage] = make_int4(0, 0, 0, 0);
+          mbar_arrive_expect_tx(&full[stage], 0u);
+          break;
+        }
         const int c0 = strip * TG_::TOUT - E;
         const int ucols = min(TG_::TLOAD, p.nx + R + 2 - c0);
         const uint32_t ubytes = (uint32_t)(((ucols + 1) & ~1) * 8);
@@ -392,6 +437,10 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
             const bool hasg = k < nin && k >= 2 * R && g1 >= p.row_lo && g1 < p.row_hi && gbytes;
             tx += (hasu ? ubytes : 0u) + (hasg ? gbytes : 0u);
           }
+#ifdef CJM_DIAG_NOTMA      // diagnostic builds only: no HBM reads, the stage completes at once
+          tx = 0;
+#endif
+          if (k0 == 0) seg_desc[stage] = make_int4(strip, ja, jb, 1);   // released by the arrive
           mbar_arrive_expect_tx(&full[stage], tx);
 #pragma unroll
           for (int r = 0; r < RPS; ++r) {
@@ -400,6 +449,9 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
             const int g1 = gin - R;
             const bool hasu = k < nin && gin >= -p.H && gin < rows + p.H;
             const bool hasg = k < nin && k >= 2 * R && g1 >= p.row_lo && g1 < p.row_hi && gbytes;
+#ifdef CJM_DIAG_NOTMA
+            continue;
+#endif
             if (hasu)
               tma_row_load(su + ((size_t)stage * RPS + r) * TG_::ROW,
                            src + (long long)(gin + p.H) * ld + (PADL - 2) + c0, ubytes, &full[stage],
@@ -411,7 +463,6 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
           ++used;
           if (++stage == p.stages) { stage = 0; phase ^= 1u; }
         }
-        uu = seg_end;
       }
     }
   } else {
@@ -429,24 +480,31 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
     ws.phase = 0;
     ws.full_a = smem_addr(full);
     ws.empty_a = smem_addr(empty);
-    for (long long uu = u_begin; uu < u_end;) {
-      const int strip = (int)(uu / p.nrows);
-      const int ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
-      const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
-      const int jb = ja + (int)(seg_end - uu);
+    for (;;) {
+      // the next segment's descriptor arrives with its first stage
+      mbar_wait_a(ws.full_a + 8u * ws.stage, ws.phase);
+      const int4 d = seg_desc[ws.stage];
+      if (!d.w) break;
+      const int strip = d.x, ja = d.y, jb = d.z;
       const int c0 = strip * TG_::TOUT - E;
-      // FAST per warp: its window holds no ghost / padding column and the
-      // segment touches no ghost row
+      // fast mode per warp (FM above): no ghost / padding column in its window
+      // (2 if the segment also touches no ghost row, else 1), or 0.  A CTA
+      // whose range starts at the top or ends at the bottom of a strip (every
+      // CTA that crosses a strip boundary) thus checks rows, not nodes: with
+      // node checks such CTAs ran 28% longer than the rest
+      // (profiles/r01_v7_cta_times.jsonl).
       const int cw = c0 + warp * WG::WOUT;
-      const bool fast = ja - K * R >= p.row_lo && jb + K * R <= p.row_hi && cw >= 0 &&
-                        cw + WG::WSPAN <= p.nx;
-      if (fast)
-        warp_segment<STENCIL, NW, K, C, RPS, REDUCE, STORE, true>(ws, p, su, sg, dst, ja, jb, c0,
-                                                                  warp, lane, acc_s, acc_m);
+      const bool fastc = cw >= 0 && cw + WG::WSPAN <= p.nx;
+      const bool fastr = ja - K * R >= p.row_lo && jb + K * R <= p.row_hi;
+      if (fastc && fastr)
+        warp_segment<STENCIL, NW, K, C, RPS, REDUCE, STORE, 2>(ws, p, su, sg, dst, ja, jb, c0, warp,
+                                                               lane, acc_s, acc_m);
+      else if (fastc)
+        warp_segment<STENCIL, NW, K, C, RPS, REDUCE, STORE, 1>(ws, p, su, sg, dst, ja, jb, c0, warp,
+                                                               lane, acc_s, acc_m);
       else
-        warp_segment<STENCIL, NW, K, C, RPS, REDUCE, STORE, false>(ws, p, su, sg, dst, ja, jb, c0,
-                                                                   warp, lane, acc_s, acc_m);
-      uu = seg_end;
+        warp_segment<STENCIL, NW, K, C, RPS, REDUCE, STORE, 0>(ws, p, su, sg, dst, ja, jb, c0, warp,
+                                                               lane, acc_s, acc_m);
     }
   }
 
@@ -469,6 +527,20 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
   }
 
   __syncthreads();
+#ifdef CJM_DIAG_TIMES
+  if (!REDUCE && tid == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    reinterpret_cast<unsigned long long*>(p.partials)[2 * blockIdx.x] = t_start;
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const long long useg = (long long)blockIdx.x * p.units / gridDim.x;   // first unit
+    const long long ueg = (long long)(blockIdx.x + 1) * p.units / gridDim.x;
+    const unsigned long long nseg = (unsigned long long)((ueg - 1) / p.nrows - useg / p.nrows + 1);
+    reinterpret_cast<unsigned long long*>(p.partials)[2 * blockIdx.x + 1] =
+        (t_end - t_start) | ((unsigned long long)smid << 40) | (nseg << 52);
+  }
+#endif
   if (tid == 0) {
     __threadfence();
     const unsigned int t = atomicAdd(&p.state->ticket, 1u);
@@ -505,6 +577,7 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
         p.state->cur = cur ^ 1u;
       }
       p.state->ticket = 0u;
+      p.state->next_chunk = 0u;
       __threadfence();
     }
   }

@@ -48,6 +48,7 @@ if __name__ == "__main__":
     ap.add_argument("--variants", type=lambda v: [int(x) for x in v.split(",")], default=[3, 4])
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--warps", type=int, default=0)
+    ap.add_argument("--chunk-rows", type=int, default=0)
     ap.add_argument("--stages-list", type=lambda v: [int(x) for x in v.split(",")], default=[4, 8, 12])
     ap.add_argument("--cps-list", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
     a = ap.parse_args()
@@ -68,4 +69,4 @@ if __name__ == "__main__":
     else:
         print(json.dumps(run(a.config, a.count, a.warm, tile_w=a.tile_w, stages=a.stages,
                              ctas_per_sm=a.ctas_per_sm, temporal_k=a.temporal_k, variant=a.variant,
-                             warps=a.warps)))
+                             warps=a.warps, chunk_rows=a.chunk_rows)))

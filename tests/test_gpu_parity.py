@@ -97,6 +97,29 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
         assert_field_parity(host(ud), u, r)
 
 
+@pytest.mark.parametrize("stencil", (5, 9, 17))
+@pytest.mark.parametrize("variant,K", [(7, 1), (7, 2), (7, 4), (4, 2), (5, 3), (6, 1)])
+@pytest.mark.parametrize("chunk_rows", (1, 7, 64))
+def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows):
+    """Hot launches whose CTAs take (strip, chunk_rows rows) work items from a
+    device counter: same field as the oracle, sweep by sweep."""
+    if stencil == 17 and (K > 2 or (K == 2 and variant in (4, 6))):
+        pytest.skip("17-point warp-tiled kernels: K=1, or K=2 with 2 columns/lane")
+    r = oracle.reach(stencil)
+    nx, ny, count = 1030, 515, 9
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=17)
+    with cjm.Plan(stencil, nx, ny, h, 1e-8, temporal_k=K, variant=variant, chunk_rows=chunk_rows,
+                  resident=-1, graph_chunk=2) as plan:
+        w = plan.info()["weights"]
+        ud = dev(u0)
+        plan.sweeps(dev(b), ud, 2, count)
+    g = oracle.rhs_to_g(stencil, h, b)
+    u = u0
+    for k in range(count):
+        u = oracle.sweep(stencil, u, g, w[(2 + k) % len(w)])
+    assert_field_parity(host(ud), u, r)
+
+
 @pytest.mark.parametrize("cfg", [dict(tile_w=256, stages=4, ctas_per_sm=1),
                                  dict(tile_w=512, stages=16, ctas_per_sm=3),
                                  dict(tile_w=256, stages=32, ctas_per_sm=2, graph_chunk=7, variant=3),
@@ -112,7 +135,10 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
                                  dict(variant=7, temporal_k=1, stages=8, ctas_per_sm=3),
                                  dict(variant=7, warps=5, temporal_k=4, stages=6),
                                  dict(variant=7, warps=7, temporal_k=2, stages=3),
-                                 dict(variant=7, warps=4, temporal_k=3, stages=5, ctas_per_sm=1)])
+                                 dict(variant=7, warps=4, temporal_k=3, stages=5, ctas_per_sm=1),
+                                 dict(variant=7, temporal_k=4, chunk_rows=24),
+                                 dict(variant=7, temporal_k=3, chunk_rows=-1),
+                                 dict(variant=4, temporal_k=2, chunk_rows=100, ctas_per_sm=1)])
 def test_launch_configuration_does_not_change_result(cfg):
     nx, ny = 777, 301
     u0, b, h = inputs.test_problem(nx, ny, 1, init="random", seed=5)
