@@ -5,16 +5,22 @@
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcjm.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("cjm.cu", "schedule.cpp", "pool.cpp", "mask_bounds.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("sweep.cuh", "sweep_v4.cuh", "resident.cuh", "mask.cuh", "internal.h")] + \
-    [os.path.join(ROOT, "include", "cjm.h")]
+SOURCES = [os.path.join(CSRC, f) for f in (
+    "cjm.cu", "kernels_v3.cu", "kernels_v4_5.cu", "kernels_v4_9.cu", "kernels_v4_17.cu",
+    "schedule.cpp", "pool.cpp", "mask_bounds.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in (
+    "sweep.cuh", "sweep_v4.cuh", "kernels.h", "kernels_v4.cuh", "resident.cuh", "mask.cuh",
+    "internal.h")] + [os.path.join(ROOT, "include", "cjm.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -41,13 +47,31 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
         return target
     inc, lib = nccl_dirs()
     tmp = target + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
-           "-Xcompiler", "-fPIC,-ffp-contract=off", "-fmad=false",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *[f"-D{d}" for d in defines], *SOURCES, "-o", tmp,
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
-    subprocess.check_call(cmd)
+    objdir = tempfile.mkdtemp(prefix="cjm_build_")
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-fmad=false",
+              "-Xptxas", "-v" if verbose else "-O3",
+              "-I", os.path.join(ROOT, "include"), "-I", inc, *[f"-D{d}" for d in defines]]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        r = subprocess.run([*common, "-c", src, "-o", obj], capture_output=True, text=True)
+        return src, obj, r
+
+    try:
+        # one nvcc per translation unit, in parallel (the sweep-kernel
+        # instantiations are spread over kernels_*.cu)
+        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            results = list(ex.map(compile_one, SOURCES))
+        for src, _, r in results:
+            if verbose or r.returncode:
+                sys.stderr.write(r.stdout + r.stderr)
+            if r.returncode:
+                raise subprocess.CalledProcessError(r.returncode, f"nvcc -c {src}")
+        subprocess.check_call([nvcc(), *ARCH, "-shared", *[o for _, o, _ in results], "-o", tmp,
+                               "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"])
+    finally:
+        shutil.rmtree(objdir, ignore_errors=True)
     os.replace(tmp, target)
     return target
 

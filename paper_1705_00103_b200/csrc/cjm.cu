@@ -28,10 +28,43 @@
 
 #include "../../include/cjm.h"
 #include "internal.h"
-#include "sweep.cuh"
-#include "sweep_v4.cuh"
+#include "kernels.h"
 #include "resident.cuh"
 #include "mask.cuh"
+
+namespace cjm {
+
+// max |u - u_ref| over the interior of an iterate buffer (the paper's "real
+// error"), NaN-propagating.  The maximum of non-negative doubles is
+// the maximum of their bit patterns, so one atomicMax per warp on the bits is
+// exact and order-free.
+__global__ void cjm_error_kernel(const double* buf, long long ld, int H, const double* ref,
+                                 long long ld_ref, int nx, int rows, unsigned long long* out_bits) {
+  const long long total = (long long)nx * rows;
+  double m = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long j = e / nx, i = e - j * nx;
+    const double d = fabs(__dsub_rn(buf[(j + H) * ld + PADL + i], ref[j * ld_ref + i]));
+    m = nan_max(m, d);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, (unsigned long long)__double_as_longlong(m));
+}
+
+// g = gscale * b in place on the interior of the internal g buffer (row a5).
+__global__ void cjm_scale_kernel(double* g, long long ld, int nx, int rows, double gscale) {
+  const long long total = (long long)nx * rows;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long j = e / nx, i = e - j * nx;
+    double* q = g + j * ld + PADL + i;
+    *q = __dmul_rn(gscale, *q);
+  }
+}
+
+}  // namespace cjm
 
 namespace {
 
@@ -87,101 +120,22 @@ void set_error(const char* what, const char* msg) {
     if (s_ != CJM_OK) return s_;          \
   } while (0)
 
-enum Mode { MODE_HOT = 0, MODE_CHECK = 1, MODE_RESID = 2 };
+using cjm::MODE_HOT;
+using cjm::MODE_CHECK;
+using cjm::MODE_RESID;
+using cjm::KernelFn;
 
-using KernelFn = void (*)(const cjm::SweepParams);
-
-template <int ST, int NT, int K>
-KernelFn pick_mode(int mode) {
-  switch (mode) {
-    case MODE_HOT: return cjm::cjm_sweep_kernel<ST, NT, K, false, true>;
-    case MODE_CHECK: return cjm::cjm_sweep_kernel<ST, NT, K, true, true>;
-    default: return cjm::cjm_sweep_kernel<ST, NT, 1, true, false>;
-  }
-}
-
-template <int ST, int NT>
-KernelFn pick_k(int K, int mode) {
-  switch (K) {
-    case 1: return pick_mode<ST, NT, 1>(mode);
-    case 2: return pick_mode<ST, NT, 2>(mode);
-    case 3: return pick_mode<ST, NT, 3>(mode);
-    default: return pick_mode<ST, NT, 4>(mode);
-  }
-}
-
-template <int ST>
-KernelFn pick_nt(int NT, int K, int mode) {
-  return NT == 256 ? pick_k<ST, 256>(K, mode) : pick_k<ST, 128>(K, mode);
-}
-
-// warp-tiled variant (sweep_v4.cuh), 4 consumer warps, C columns per lane,
-// RPS input rows per TMA ring stage
-template <int ST, int K, int C, int RPS, int NW = 4>
-KernelFn pick_mode_v4(int mode) {
-  switch (mode) {
-    case MODE_HOT: return cjm::cjm_sweep_kernel_v4<ST, NW, K, C, false, true, RPS>;
-    case MODE_CHECK: return cjm::cjm_sweep_kernel_v4<ST, NW, K, C, true, true, RPS>;
-    default: return cjm::cjm_sweep_kernel_v4<ST, NW, 1, C, true, false, RPS>;
-  }
-}
-
-// the 17-point warp-tiled kernel with K >= 2 does not fit the register file
-// (5-row rings of 4 columns x 3 arrays per level): not instantiated, the plan
-// uses the shared-line variant there
-template <int ST, int C, int RPS, int NW = 4>
-KernelFn pick_k_v4(int K, int mode) {
-  if constexpr (ST == 17 && C == 4) {
-    return K == 1 ? pick_mode_v4<ST, 1, C, RPS, NW>(mode) : nullptr;
-  } else if constexpr (ST == 17) {
-    return K == 1 ? pick_mode_v4<ST, 1, C, RPS, NW>(mode)
-                  : K == 2 ? pick_mode_v4<ST, 2, C, RPS, NW>(mode) : nullptr;
-  } else {
-    switch (K) {
-      case 1: return pick_mode_v4<ST, 1, C, RPS, NW>(mode);
-      case 2: return pick_mode_v4<ST, 2, C, RPS, NW>(mode);
-      case 3: return pick_mode_v4<ST, 3, C, RPS, NW>(mode);
-      default: return pick_mode_v4<ST, 4, C, RPS, NW>(mode);
+// nw: consumer warps per CTA (variant 7 only: 4, 5 or 7).  The instantiations
+// live in kernels_*.cu (compiled in parallel).
+KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode, int nw = 4) {
+  if (variant >= 4) {
+    switch (stencil) {
+      case 5: return cjm::pick_sweep_v4_5(variant, K, mode, nw);
+      case 9: return cjm::pick_sweep_v4_9(variant, K, mode, nw);
+      default: return cjm::pick_sweep_v4_17(variant, K, mode, nw);
     }
   }
-}
-
-template <int C, int MULTI, int NW = 4>   // MULTI: 2r+1 rows per ring stage
-KernelFn pick_st_v4(int stencil, int K, int mode) {
-  switch (stencil) {
-    case 5: return pick_k_v4<5, C, MULTI ? 3 : 1, NW>(K, mode);
-    case 9: return pick_k_v4<9, C, MULTI ? 3 : 1, NW>(K, mode);
-    default: return pick_k_v4<17, C, MULTI ? 5 : 1, NW>(K, mode);
-  }
-}
-
-// nw: consumer warps per CTA (variant 7 only: 4, 5 or 7)
-KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode, int nw = 4) {
-#ifdef CJM_EXPERIMENT_9PT_V7
-  // measurement builds (build.build(defines=..., out=...)): only the 9-point
-  // variant-7 kernels, so an experiment compiles in seconds
-  if (stencil != 9 || variant != 7) return nullptr;
-  switch (nw) {
-    case 5: return pick_k_v4<9, 2, 3, 5>(K, mode);
-    case 7: return pick_k_v4<9, 2, 3, 7>(K, mode);
-    default: return pick_k_v4<9, 2, 3, 4>(K, mode);
-  }
-#else
-  switch (variant) {      // warp-tiled: 4 / 2 columns per lane, 1 / 2r+1 rows per stage
-    case 4: return pick_st_v4<4, 0>(stencil, K, mode);
-    case 5: return pick_st_v4<2, 0>(stencil, K, mode);
-    case 6: return pick_st_v4<4, 1>(stencil, K, mode);
-    case 7:
-      return nw == 5 ? pick_st_v4<2, 1, 5>(stencil, K, mode)
-           : nw == 7 ? pick_st_v4<2, 1, 7>(stencil, K, mode) : pick_st_v4<2, 1, 4>(stencil, K, mode);
-    default: break;
-  }
-  switch (stencil) {
-    case 5: return pick_nt<5>(NT, K, mode);
-    case 9: return pick_nt<9>(NT, K, mode);
-    default: return pick_nt<17>(NT, K, mode);
-  }
-#endif
+  return cjm::pick_sweep_v3(stencil, NT, K, mode);
 }
 
 // halo columns lost per side by K-1 on-chip levels (mirror of TileGeom::E)

@@ -557,34 +557,4 @@ cjm_sweep_kernel(const SweepParams p) {
   }
 }
 
-// max |u - u_ref| over the interior of an iterate buffer (the paper's "real
-// error"), NaN-propagating.  The maximum of non-negative doubles is
-// the maximum of their bit patterns, so one atomicMax per warp on the bits is
-// exact and order-free.
-__global__ void cjm_error_kernel(const double* buf, long long ld, int H, const double* ref,
-                                 long long ld_ref, int nx, int rows, unsigned long long* out_bits) {
-  const long long total = (long long)nx * rows;
-  double m = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long j = e / nx, i = e - j * nx;
-    const double d = fabs(__dsub_rn(buf[(j + H) * ld + PADL + i], ref[j * ld_ref + i]));
-    m = nan_max(m, d);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, (unsigned long long)__double_as_longlong(m));
-}
-
-// g = gscale * b in place on the interior of the internal g buffer (row a5).
-__global__ void cjm_scale_kernel(double* g, long long ld, int nx, int rows, double gscale) {
-  const long long total = (long long)nx * rows;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long j = e / nx, i = e - j * nx;
-    double* q = g + j * ld + PADL + i;
-    *q = __dmul_rn(gscale, *q);
-  }
-}
-
 }  // namespace cjm
