@@ -60,7 +60,8 @@ def test_mask_sweeps_bitwise(kind, nx, ny, first, count):
     u[1:-1, 1:-1] = inputs.uniform_pm1(11 + nx, nx * ny).reshape(ny, nx)
     kmin, kmax = bounds(mk)
     with cjm.MaskPlan(nx, ny, kmin, kmax, 1e-8, mask=dev(mk)) as plan:
-        w = plan.info()["weights"]
+        _, w = oracle_weights(kmin, kmax, 1e-8)     # the oracle's own inputs
+        assert np.array_equal(plan.info()["weights"], w)
         ud = torch.from_numpy(u.copy()).cuda()
         plan.sweeps(torch.from_numpy(b).cuda(), ud, first, count)
         got = ud.cpu().numpy()
@@ -139,7 +140,7 @@ def test_mask_set_required_and_replaceable():
             plan.sweeps(bd, torch.from_numpy(u0.copy()).cuda(), 0, 1)
         assert e.value.name == "CJM_ERR_INVALID_ARG"
         plan.mask_set(dev(mk))
-        w0 = float(plan.info()["weights"][0])
+        w0 = float(oracle_weights(kmin, kmax, 1e-8)[1][0])
         mk2 = {k: v * 3.0 for k, v in masks.bipolar_problem(48, 40)[0].items()}
         plan.mask_set(dev(mk2))              # a new operator, same plan
         ud = torch.from_numpy(u0.copy()).cuda()
@@ -164,7 +165,8 @@ def test_mask_sweeps_bitwise_at_bench_size(kind):
     u[1:-1, 1:-1] = inputs.uniform_pm1(3, n * n).reshape(n, n)
     kmin, kmax = 1e-6, 2.0 - 1e-6           # bounds only enter through the weights
     with cjm.MaskPlan(n, n, kmin, kmax, 1e-8, mask=dev(mk)) as plan:
-        w = plan.info()["weights"]
+        _, w = oracle_weights(kmin, kmax, 1e-8)
+        assert np.array_equal(plan.info()["weights"], w)
         ud = torch.from_numpy(u.copy()).cuda()
         plan.sweeps(torch.from_numpy(b).cuda(), ud, 7, 3)
         got = ud.cpu().numpy()

@@ -39,6 +39,14 @@ def host(t) -> np.ndarray:
     return t.cpu().numpy()
 
 
+def oracle_weights(stencil: int, nx: int, ny: int, plan, tol: float = 1e-8) -> np.ndarray:
+    """The oracle's own schedule (no oracle input comes from the CUDA path);
+    the plan must hold the same weights, bitwise."""
+    w = oracle.schedule(stencil, nx, ny, tol)["w"]
+    assert np.array_equal(plan.info()["weights"], w)
+    return w
+
+
 def assert_field_parity(got: np.ndarray, want: np.ndarray, r: int):
     gi, wi = got[r:-r, r:-r], want[r:-r, r:-r]
     scale = max(np.max(np.abs(wi)), 1e-300)
@@ -62,7 +70,7 @@ def test_one_sweep_bitwise(stencil, nx, ny, tile_w, variant):
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=inputs.SEED_BASE + nx + 7 * ny)
     kw = dict(temporal_k=1) if (stencil == 17 and variant >= 4) else {}
     with cjm.Plan(stencil, nx, ny, h, 1e-8, tile_w=tile_w, variant=variant, **kw) as plan:
-        w = plan.info()["weights"]
+        w = oracle_weights(stencil, nx, ny, plan)
         g = oracle.rhs_to_g(stencil, h, b)
         for first in (0, 1, plan.P - 1):
             ud = dev(u0)
@@ -87,7 +95,7 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=3)
     with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=4, temporal_k=temporal_k,
                   variant=variant, resident=-1) as plan:
-        w = plan.info()["weights"]
+        w = oracle_weights(stencil, nx, ny, plan)
         ud = dev(u0)
         plan.sweeps(dev(b), ud, 5, count)
         g = oracle.rhs_to_g(stencil, h, b)
@@ -110,7 +118,7 @@ def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows):
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=17)
     with cjm.Plan(stencil, nx, ny, h, 1e-8, temporal_k=K, variant=variant, chunk_rows=chunk_rows,
                   resident=-1, graph_chunk=2) as plan:
-        w = plan.info()["weights"]
+        w = oracle_weights(stencil, nx, ny, plan)
         ud = dev(u0)
         plan.sweeps(dev(b), ud, 2, count)
     g = oracle.rhs_to_g(stencil, h, b)
@@ -307,6 +315,29 @@ def test_solve_matches_stored_oracle_digest(name, temporal_k, resident):  # noqa
     assert hashlib.sha256(np.ascontiguousarray(u, dtype="<f8").tobytes()).hexdigest() == rec["sha256"]
 
 
+@pytest.mark.parametrize("stencil,n,first", [(9, 16384, 41471), (17, 8192, 20001)])
+def test_full_size_segment_bitwise(stencil, n, first):
+    """BASELINE full sizes (the 16384^2 target has no stored full-solve digest:
+    its oracle solve takes hours) in the launch configuration bench.py times
+    (default plan: K fused sweeps, dynamic work items, boundary fast modes):
+    a segment of scheduled sweeps from a random iterate, whole field bitwise
+    equal to the oracle's."""
+    r = oracle.reach(stencil)
+    free = torch.cuda.mem_get_info()[0]
+    if free < 8 * (n + 2 * r) * (n + 2 * r) * 8:
+        pytest.skip("not enough device memory")
+    u0, b, h = inputs.test_problem(n, n, r, init="random", seed=23)
+    with cjm.Plan(stencil, n, n, h, 1e-8) as plan:
+        w = oracle_weights(stencil, n, n, plan)
+        count = 2 * plan.info()["temporal_k"] + 1   # two fused launches + a remainder sweep
+        ud = dev(u0)
+        plan.sweeps(dev(b), ud, first, count)
+        got = host(ud)
+        del ud
+    want = oracle.sweeps(stencil, u0, oracle.rhs_to_g(stencil, h, b), w, first, count)
+    assert_field_parity(got, want, r)
+
+
 # ------------------------------------------------------------ real-error stop (NEXT-3)
 @pytest.mark.parametrize("stencil,n,real_tol", [(17, 127, 1e-8), (5, 63, 1e-6), (9, 100, 1e-4)])
 def test_real_error_stop_matches_oracle_cycles(stencil, n, real_tol):
@@ -359,7 +390,7 @@ def test_resident_segment_bitwise(stencil, nx, ny, count):
         assert e.name == "CJM_ERR_INVALID_ARG" and nx * ny >= 1024 * 1024
         pytest.skip("grid does not fit in shared memory")
     with plan:
-        w = plan.info()["weights"]
+        w = oracle_weights(stencil, nx, ny, plan)
         ud = dev(u0)
         rep = plan.sweeps(dev(b), ud, 3, count)
         assert rep["resident"] == 1 and rep["hot_launches"] == 1
