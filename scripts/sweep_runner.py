@@ -49,6 +49,7 @@ if __name__ == "__main__":
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--chunk-rows", type=int, default=0)
+    ap.add_argument("--resident", type=int, default=-1)
     ap.add_argument("--stages-list", type=lambda v: [int(x) for x in v.split(",")], default=[4, 8, 12])
     ap.add_argument("--cps-list", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
     a = ap.parse_args()
@@ -69,4 +70,4 @@ if __name__ == "__main__":
     else:
         print(json.dumps(run(a.config, a.count, a.warm, tile_w=a.tile_w, stages=a.stages,
                              ctas_per_sm=a.ctas_per_sm, temporal_k=a.temporal_k, variant=a.variant,
-                             warps=a.warps, chunk_rows=a.chunk_rows)))
+                             warps=a.warps, chunk_rows=a.chunk_rows, resident=a.resident)))

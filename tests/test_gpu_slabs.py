@@ -77,7 +77,7 @@ def test_slabs_bitwise_equal_single_domain(world, stencil, nx, ny, band_split):
 
 @pytest.mark.parametrize("world,stencil,nx,ny", [(2, 9, 300, 257), (4, 17, 130, 97), (3, 5, 200, 64),
                                                  (8, 9, 513, 200)])
-@pytest.mark.parametrize("K,variant", [(2, 0), (3, 3), (2, 3), (4, 0), (2, 5), (2, 6), (3, 7)])
+@pytest.mark.parametrize("K,variant", [(2, 0), (3, 3), (2, 3), (4, 0), (2, 5), (2, 6), (3, 7), (2, 77)])
 @pytest.mark.parametrize("band_split", (0, 1))
 def test_deep_halo_slabs_bitwise(world, stencil, nx, ny, K, variant, band_split):
     """K sweeps fused per launch across slabs: H = K r deep halos (u with H
@@ -90,7 +90,9 @@ def test_deep_halo_slabs_bitwise(world, stencil, nx, ny, K, variant, band_split)
     plans = []
     for g in range(world):
         kw = dict(world_size=world, rank=g, external_halo=1, temporal_k=K, band_split=band_split)
-        if variant:
+        if variant == 77:      # variant 7 with small dynamic work items (band launches too)
+            kw.update(variant=7, chunk_rows=5)
+        elif variant:
             kw["variant"] = variant
         if stencil == 17 and (variant == 0 or (variant in (4, 6) and K > 1) or
                               (variant in (5, 7) and K > 2)):
