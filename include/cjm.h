@@ -128,11 +128,13 @@ typedef struct {
     int warps;             /* variant 7 only: consumer warps per CTA, 4, 5 or 7
                               (0 = the count that keeps the most consumer warps
                               resident per SM) */
-    int chunk_rows;        /* warp-tiled variants: rows per work item that the CTAs of a
-                              non-reducing launch take from a device counter (dynamic load
-                              balancing); 0 = automatic (256 / 128 rows when every CTA
-                              gets >= 2048 / 1024 rows, else static), -1 = static
-                              contiguous ranges per CTA */
+    int chunk_rows;        /* warp-tiled variants, non-reducing launches: every CTA
+                              streams a static range of 80% of its share of the
+                              (strip, row) units, the last 20% go out in work items of
+                              chunk_rows units that the CTAs take from a device counter
+                              (dynamic load balancing); 0 = automatic (1/8 of a CTA's
+                              share, 16..128), -1 = static ranges only.  The fraction
+                              can be overridden with CJM_DYN_PCT (0..100) for tuning */
 } cjm_options;
 
 typedef struct {

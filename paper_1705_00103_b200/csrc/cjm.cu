@@ -206,6 +206,7 @@ struct cjm_plan_s {
   int nw = 4;        // consumer warps per CTA (warp-tiled)
   int chunk_rows = -1;  // warp-tiled hot launches: rows per dynamically scheduled work item
                         // (0: static ranges, -1: chosen per launch)
+  int dyn_pct = 20;     // percent of the units scheduled dynamically (CJM_DYN_PCT)
   int band_split = 0;  // split hot sweeps into boundary / interior bands even without NCCL
   // resident (whole grid in shared memory) hot path
   int resident = 0, res_ctas = 0, res_rows = 0;
@@ -320,17 +321,25 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int ro
   sp.units = nstrips * nrows;
   const int grid = (int)std::min<long long>(pl->nctas, sp.units);
   // Dynamic balancing for hot launches of the warp-tiled kernels only (a
-  // reducing launch keeps static per-CTA ranges: bitwise-reproducible sums).
-  // Auto: only when every CTA gets >= ~8 work items, since each item re-reads
-  // and recomputes 2 K r halo rows (measured, profiles/r01_v7_chunks.jsonl:
-  // 16384^2 K=4 330 vs 415 us per sweep with 256-row items; 4096^2, 208 rows
-  // per CTA, is faster static).
+  // reducing launch keeps static per-CTA ranges: bitwise-reproducible sums):
+  // a static per-CTA range over the first 80% of the units, the last 20% in
+  // work items of 1/8 of a CTA's share (16..128 units) from a device counter
+  // -- the CTAs on faster SMs take more of them.  Each item re-reads and
+  // recomputes 2 K r halo rows.  Measured (profiles/r01_v7_chunks.jsonl): 9-pt
+  // K=4 at 4096^2 24.0 vs 26.6 us per sweep static, 16384^2 325 vs 425.
   int chunk = 0;
-  if (mode == MODE_HOT && pl->variant >= 4) {
-    const long long per_cta = sp.units / std::max(grid, 1);
-    chunk = pl->chunk_rows >= 0 ? pl->chunk_rows : per_cta >= 2048 ? 256 : per_cta >= 1024 ? 128 : 0;
+  long long ustat = sp.units;
+  const long long per_cta = sp.units / std::max(grid, 1);
+  if (mode == MODE_HOT && pl->variant >= 4 &&
+      (pl->chunk_rows > 0 || (pl->chunk_rows < 0 && per_cta >= 64))) {
+    // (auto: small grids, e.g. 1024^2 with 14 rows per CTA, stay static --
+    // 21.3 vs 27.7 ms per 9-point solve)
+    chunk = pl->chunk_rows > 0 ? pl->chunk_rows
+                               : (int)std::max<long long>(16, std::min<long long>(128, per_cta / 8));
+    ustat = sp.units - sp.units * pl->dyn_pct / 100;
   }
   sp.chunk_rows = chunk;
+  sp.units_static = ustat;
   KernelFn k = pick_kernel(pl->stencil, pl->variant, pl->NT, K, mode, pl->nw);
   k<<<grid, block_threads(pl), smem_bytes(pl, K), st>>>(sp);
   CUDA_TRY(cudaGetLastError());
@@ -932,6 +941,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     pl->NT = cjm::MASK_NT;
     pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
   pl->chunk_rows = opt.chunk_rows > 0 ? opt.chunk_rows : (opt.chunk_rows < 0 ? 0 : -1);   // -1: auto
+  if (const char* e = std::getenv("CJM_DYN_PCT")) pl->dyn_pct = std::max(0, std::min(100, std::atoi(e)));
     pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : 8;
     int occ = 0;
     PLAN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -979,6 +989,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
                                                   : pl->variant >= 4 ? 8 : (pl->NT == 256 ? 12 : 4));
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
   pl->chunk_rows = opt.chunk_rows > 0 ? opt.chunk_rows : (opt.chunk_rows < 0 ? 0 : -1);   // -1: auto
+  if (const char* e = std::getenv("CJM_DYN_PCT")) pl->dyn_pct = std::max(0, std::min(100, std::atoi(e)));
   // The grid is sized for the hot kernel (persistent: ctas_per_sm per SM, all
   // resident).  Check / residual / remainder kernels may need more registers;
   // they then run the same grid in more than one wave, which is correct

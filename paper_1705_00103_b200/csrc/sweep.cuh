@@ -68,9 +68,11 @@ struct SweepParams {
   int row0, nrows;             // the band of output rows of this launch
   int stages;                  // TMA ring depth
   int advance;                 // the last CTA advances n / flips cur (last launch of a sweep)
-  int chunk_rows;              // warp-tiled kernel: > 0 = CTAs take (strip, chunk_rows rows)
-                               // work items from a device counter (dynamic balancing);
-                               // 0 = one contiguous range of (strip, row) units per CTA
+  int chunk_rows;              // warp-tiled kernel: 0 = one contiguous range of (strip, row)
+                               // units per CTA; > 0 = units [0, units_static) in static
+                               // per-CTA ranges, the rest in chunk_rows-unit work items taken
+                               // from a device counter (dynamic balancing)
+  long long units_static;
 };
 
 // ---------------------------------------------------------------- PTX helpers

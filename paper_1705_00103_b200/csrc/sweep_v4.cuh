@@ -329,8 +329,14 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
 // 17-point) keep one CTA per SM and are not capped.
 template <int STENCIL, int K, int C>
 struct V4Regs {
+#ifdef CJM_X_NW7_NOCAP   // experiment: 7 consumer warps (one CTA per SM) without the cap
+  static constexpr int value = 255;
+#elif defined(CJM_X_CAP128)   // experiment: 4 warps per sub-partition
+  static constexpr int value = 128;
+#else
   static constexpr int value =
       Point<STENCIL>::R == 1 ? ((C == 2 || K <= 2) ? 168 : 255) : ((C == 2 && K == 1) ? 168 : 255);
+#endif
 };
 
 template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE, int RPS = 1>
@@ -373,8 +379,11 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
   double* dst = (cur & 1u) ? p.buf[0] : p.buf[1];
   const long long ld = p.ld;
   const int rows = p.rows;
-  const long long u_begin = (long long)blockIdx.x * p.units / gridDim.x;
-  const long long u_end = (long long)(blockIdx.x + 1) * p.units / gridDim.x;
+  // static part of the (strip, row) units: one contiguous range per CTA; the
+  // rest [units_static, units) goes out in chunk_rows-unit items (hot launches)
+  const long long ustat = p.chunk_rows > 0 ? p.units_static : p.units;
+  const long long u_begin = (long long)blockIdx.x * ustat / gridDim.x;
+  const long long u_end = (long long)(blockIdx.x + 1) * ustat / gridDim.x;
 
   double acc_s = 0.0, acc_m = 0.0;
 
@@ -386,31 +395,23 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
       uint32_t phase = 0;
       long long used = 0;
       const uint32_t full_a = smem_addr(full), empty_a = smem_addr(empty);
-      const int cpr = p.chunk_rows > 0 ? (p.nrows + p.chunk_rows - 1) / p.chunk_rows : 1;
-      const long long nchunks = (p.units / p.nrows) * cpr;
-      long long uu = u_begin;
+      long long uu = u_begin, ue = u_end;    // current unit range
       for (;;) {
-        // ---- next segment: (strip, rows [ja, jb)), or the end marker
-        int strip = 0, ja = 0, jb = 0;
-        bool more;
-        if (p.chunk_rows > 0) {
+        // ---- next segment: (strip, rows [ja, jb)), or the end marker.  A
+        // range that spans a strip boundary yields two segments.
+        if (uu >= ue && p.chunk_rows > 0) {
           const long long c = atomicAdd(&p.state->next_chunk, 1u);
-          more = c < nchunks;
-          if (more) {
-            strip = (int)(c / cpr);
-            const int q = (int)(c - (long long)strip * cpr);
-            ja = p.row0 + q * p.chunk_rows;
-            jb = min(ja + p.chunk_rows, p.row0 + p.nrows);
-          }
-        } else {
-          more = uu < u_end;
-          if (more) {
-            strip = (int)(uu / p.nrows);
-            ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
-            const long long seg_end = min(u_end, (long long)(strip + 1) * p.nrows);
-            jb = ja + (int)(seg_end - uu);
-            uu = seg_end;
-          }
+          uu = p.units_static + c * p.chunk_rows;
+          ue = min(uu + p.chunk_rows, p.units);
+        }
+        const bool more = uu < ue;
+        int strip = 0, ja = 0, jb = 0;
+        if (more) {
+          strip = (int)(uu / p.nrows);
+          ja = p.row0 + (int)(uu - (long long)strip * p.nrows);
+          const long long seg_end = min(ue, (long long)(strip + 1) * p.nrows);
+          jb = ja + (int)(seg_end - uu);
+          uu = seg_end;
         }
         if (!more) {   // end marker: a stage without data
           if (used >= p.stages) mbar_wait_a(empty_a + 8u * stage, phase ^ 1u);
@@ -534,8 +535,7 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
     reinterpret_cast<unsigned long long*>(p.partials)[2 * blockIdx.x] = t_start;
     unsigned int smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    const long long useg = (long long)blockIdx.x * p.units / gridDim.x;   // first unit
-    const long long ueg = (long long)(blockIdx.x + 1) * p.units / gridDim.x;
+    const long long useg = u_begin, ueg = u_end;
     const unsigned long long nseg = (unsigned long long)((ueg - 1) / p.nrows - useg / p.nrows + 1);
     reinterpret_cast<unsigned long long*>(p.partials)[2 * blockIdx.x + 1] =
         (t_end - t_start) | ((unsigned long long)smid << 40) | (nseg << 52);

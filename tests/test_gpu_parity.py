@@ -108,11 +108,14 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("variant,K", [(7, 1), (7, 2), (7, 4), (4, 2), (5, 3), (6, 1)])
 @pytest.mark.parametrize("chunk_rows", (1, 7, 64))
-def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows):
-    """Hot launches whose CTAs take (strip, chunk_rows rows) work items from a
-    device counter: same field as the oracle, sweep by sweep."""
+@pytest.mark.parametrize("dyn_pct", ("20", "100"))
+def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows, dyn_pct, monkeypatch):
+    """Hot launches whose CTAs take work items of chunk_rows (strip, row)
+    units from a device counter (the default last 20% of the units, or all of
+    them): same field as the oracle, sweep by sweep."""
     if stencil == 17 and (K > 2 or (K == 2 and variant in (4, 6))):
         pytest.skip("17-point warp-tiled kernels: K=1, or K=2 with 2 columns/lane")
+    monkeypatch.setenv("CJM_DYN_PCT", dyn_pct)
     r = oracle.reach(stencil)
     nx, ny, count = 1030, 515, 9
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=17)
