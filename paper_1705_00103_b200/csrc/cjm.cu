@@ -961,24 +961,25 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   pl->ctas_per_sm = opt.ctas_per_sm > 0 ? opt.ctas_per_sm : (opt.world_size > 1 ? 3 : 4);
   // Default: the warp-tiled kernel with 2 columns per lane and 2r+1 rows per
   // TMA stage (variant 7), consumer warps per CTA chosen below.  5/9-point:
-  // four sweeps per launch from 4096^2 up, three below; 17-point: two
-  // (profiles/r01_v7_tune.jsonl: 27.3 us per 9-point sweep at 4096^2 vs 37.9
-  // for variant 4 at K = 2; 404 vs 599 at 16384^2; 167 vs 290 per 17-point
-  // sweep at 8192^2 for variant 3 at K = 1).  An explicit tile_w selects the
-  // shared-line kernel (variant 3).
+  // four sweeps per launch from 4096^2 up, three below; 17-point: three from
+  // 4096^2 up, two below (profiles/r01_v7_tune.jsonl: 27.3 us per 9-point
+  // sweep at 4096^2 vs 37.9 for variant 4 at K = 2; 404 vs 599 at 16384^2;
+  // 17-point at 8192^2: 139 us at K = 3, 155 at K = 2, 290 for variant 3 at
+  // K = 1).  An explicit tile_w selects the shared-line kernel (variant 3).
   const bool wide = stencil == 17;
   pl->NT = opt.tile_w == 512 || (opt.tile_w == 0 && wide) ? 256 : 128;
   pl->variant = opt.variant ? opt.variant : (opt.tile_w ? 3 : 7);
   pl->band_split = opt.band_split;
   pl->K = opt.temporal_k > 0 ? opt.temporal_k
-                             : (wide ? 2 : ((long long)nx * ny >= 4096LL * 4096LL ? 4 : 3));
+                             : ((long long)nx * ny >= 4096LL * 4096LL ? (wide ? 3 : 4) : (wide ? 2 : 3));
   // multi-GPU: K-fused launches need H = K r deep halos, exchanged after every
   // launch; the slab must stay thicker than 2H + 1 rows (else fall back to K=1)
   if (pl->world > 1 && nyl < 2 * pl->K * R + 1) pl->K = 1;
   if (stencil == 17 && pl->K > 1 && pl->variant >= 4) {
-    if (v4_cpl(pl->variant) == 4 || pl->K > 2) {
+    if (v4_cpl(pl->variant) == 4 || pl->K > (pl->variant == 7 ? 3 : 2)) {
       if (opt.variant >= 4) {
-        set_error("cjm_plan", "warp-tiled variants run the 17-point with temporal_k <= 2 (variants 5, 7) only");
+        set_error("cjm_plan", "warp-tiled variants run the 17-point with temporal_k <= 2 (variant 5) "
+                              "or <= 3 (variant 7) only");
         return fail(CJM_ERR_INVALID_ARG);
       }
       pl->variant = 3;

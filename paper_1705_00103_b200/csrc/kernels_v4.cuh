@@ -18,13 +18,19 @@ KernelFn pick_mode_v4(int mode) {
   }
 }
 
-// the 17-point warp-tiled kernel with K >= 2 does not fit the register file
-// (5-row rings of 4 columns x 3 arrays per level): not instantiated, the plan
-// uses the shared-line variant there
+// the 17-point warp-tiled kernel with 4 columns per lane and K >= 2 does not
+// fit the register file (5-row rings of 4 columns x 3 arrays per level), nor
+// with 2 columns beyond K = 2 (one row per stage) / K = 3 (2r+1 rows per
+// stage, 255 registers): not instantiated, the plan uses the shared-line
+// variant there
 template <int ST, int C, int RPS, int NW = 4>
 KernelFn pick_k_v4(int K, int mode) {
   if constexpr (ST == 17 && C == 4) {
     return K == 1 ? pick_mode_v4<ST, 1, C, RPS, NW>(mode) : nullptr;
+  } else if constexpr (ST == 17 && RPS > 1) {   // variant 7: up to K = 3
+    return K == 1 ? pick_mode_v4<ST, 1, C, RPS, NW>(mode)
+           : K == 2 ? pick_mode_v4<ST, 2, C, RPS, NW>(mode)
+           : K == 3 ? pick_mode_v4<ST, 3, C, RPS, NW>(mode) : nullptr;
   } else if constexpr (ST == 17) {
     return K == 1 ? pick_mode_v4<ST, 1, C, RPS, NW>(mode)
                   : K == 2 ? pick_mode_v4<ST, 2, C, RPS, NW>(mode) : nullptr;

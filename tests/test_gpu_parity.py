@@ -89,8 +89,9 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
     """A run of sweeps through the CUDA-graph hot loop (spans several graph
     chunks when count > graph_chunk), K sweeps fused per launch (temporal
     blocking), every kernel variant, vs the oracle sweep by sweep."""
-    if stencil == 17 and ((variant in (4, 6) and temporal_k > 1) or (variant in (5, 7) and temporal_k > 2)):
-        pytest.skip("17-point warp-tiled kernels: K=1 (4 columns/lane) or K<=2 (2 columns/lane)")
+    if stencil == 17 and ((variant in (4, 6) and temporal_k > 1) or (variant == 5 and temporal_k > 2)
+                          or (variant == 7 and temporal_k > 3)):
+        pytest.skip("17-point warp-tiled kernels: K=1 (4 columns/lane), K<=2 (variant 5), K<=3 (7)")
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=3)
     with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=4, temporal_k=temporal_k,
@@ -106,15 +107,15 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
 
 
 @pytest.mark.parametrize("stencil", (5, 9, 17))
-@pytest.mark.parametrize("variant,K", [(7, 1), (7, 2), (7, 4), (4, 2), (5, 3), (6, 1)])
+@pytest.mark.parametrize("variant,K", [(7, 1), (7, 2), (7, 3), (7, 4), (4, 2), (5, 3), (6, 1)])
 @pytest.mark.parametrize("chunk_rows", (1, 7, 64))
 @pytest.mark.parametrize("dyn_pct", ("20", "100"))
 def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows, dyn_pct, monkeypatch):
     """Hot launches whose CTAs take work items of chunk_rows (strip, row)
     units from a device counter (the default last 20% of the units, or all of
     them): same field as the oracle, sweep by sweep."""
-    if stencil == 17 and (K > 2 or (K == 2 and variant in (4, 6))):
-        pytest.skip("17-point warp-tiled kernels: K=1, or K=2 with 2 columns/lane")
+    if stencil == 17 and ((K > 1 and variant in (4, 6)) or (K > 2 and variant == 5) or K > 3):
+        pytest.skip("17-point warp-tiled kernels: K=1 (4 columns/lane), K<=2 (variant 5), K<=3 (7)")
     monkeypatch.setenv("CJM_DYN_PCT", dyn_pct)
     r = oracle.reach(stencil)
     nx, ny, count = 1030, 515, 9
@@ -186,7 +187,7 @@ def test_solve_matches_oracle(stencil, n, init, temporal_k, variant, resident):
     u0, b, h = inputs.test_problem(n, n, r, init=init)
     uo, ro = oracle.solve(stencil, h, 1e-8, b, u0)
     if stencil == 17 and variant >= 4 and temporal_k > 1:
-        variant = {4: 0, 5: 5, 6: 0, 7: 7}[variant] if temporal_k <= 2 else 0
+        variant = {4: 0, 5: 5 if temporal_k <= 2 else 0, 6: 0, 7: 7 if temporal_k <= 3 else 0}[variant]
     with cjm.Plan(stencil, n, n, h, 1e-8, temporal_k=temporal_k, variant=variant,
                   resident=resident) as plan:
         assert plan.info()["resident"] == (1 if resident == 1 else 0)

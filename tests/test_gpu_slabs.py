@@ -95,7 +95,7 @@ def test_deep_halo_slabs_bitwise(world, stencil, nx, ny, K, variant, band_split)
         elif variant:
             kw["variant"] = variant
         if stencil == 17 and (variant == 0 or (variant in (4, 6) and K > 1) or
-                              (variant in (5, 7) and K > 2)):
+                              (variant == 5 and K > 2) or (variant in (7, 77) and K > 3)):
             kw["variant"] = 3
         plans.append(cjm.Plan(stencil, nx, ny, h, 1e-8, **kw))
     H = plans[0].ghost_rows
