@@ -1060,7 +1060,12 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     set_error("cjm_plan", "sweep kernel does not fit on an SM with these options");
     return fail(CJM_ERR_INVALID_ARG);
   }
-  pl->nctas = nsm * std::min(occ_min, pl->ctas_per_sm);
+  // multi-GPU with NCCL: two SMs are left to the NCCL kernels of the halo
+  // exchange, which overlaps the interior band launch (a persistent grid on
+  // every SM would leave them no slot: the warp-tiled kernels fill the
+  // register file); the dynamic work items absorb the lost SMs
+  const int reserve = (pl->world > 1 && !opt.external_halo && nsm > 8) ? 2 : 0;
+  pl->nctas = (nsm - reserve) * std::min(occ_min, pl->ctas_per_sm);
   }
 
   // ---- resident (shared-memory) hot path: single GPU, whole grid fits in the
