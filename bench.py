@@ -43,6 +43,10 @@ CONFIGS = {
     "cjm5_1024": (5, 1024, 1024, 1e-8, "configs[1]: 5-point at 1024^2"),
     "cjm17_1024": (17, 1024, 1024, 1e-8, "17-point at 1024^2 (tab:tab01 size)"),
     "cjm9_64": (9, 64, 64, 1e-8, "configs[0]: 9-point at 64^2"),
+    # configs[4]: 9-point at 32768 columns; weak = 4096-row slab per GPU (ny = 4096 G),
+    # strong = the whole 32768^2 grid (one GPU holds it: 3 x 8.6 GB; ~4 min per solve)
+    "cjm9_32768w": (9, 32768, 4096, 1e-8, "configs[4] weak: 9-point, 32768 x 4096 slab per GPU"),
+    "cjm9_32768": (9, 32768, 32768, 1e-8, "configs[4] strong: 9-point at 32768^2"),
 }
 METRIC = "GLUPS (fp64 lattice updates/s) and time-to-tol vs HBM roofline"
 
