@@ -66,12 +66,23 @@ def source(x: np.ndarray, y: np.ndarray) -> np.ndarray:
     return -(X * X + Y * Y) * np.exp(np.multiply.outer(y, x))
 
 
+def source_laplacian(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Delta f for f of `source`: e^{xy} (-4 - 8xy - (x^2 + y^2)^2)."""
+    X = x[None, :]
+    Y = y[:, None]
+    r2 = X * X + Y * Y
+    return (-4.0 - 8.0 * X * Y - r2 * r2) * np.exp(np.multiply.outer(y, x))
+
+
 def test_problem(nx: int, ny: int, r: int, *, h: float | None = None,
-                 init: str = "zero", seed: int | None = None):
+                 init: str = "zero", seed: int | None = None, rhs: str = "pointwise"):
     """Returns (u0, b, h).
 
     u0: (ny + 2r, nx + 2r) float64, ghosts = -e^{xy}, interior = init guess.
-    b : (ny, nx) float64, the source sampled at the interior nodes.
+    b : (ny, nx) float64, the source sampled at the interior nodes
+        (rhs="pointwise"), or with the Mehrstellen correction
+        b = f + (h^2/12) Delta f (rhs="mehrstellen"), which makes the compact
+        9-point alpha=2/3 stencil fourth order (DESIGN R7; SURVEY [V7]).
     """
     if h is None:
         h = grid_h(nx, ny)
@@ -87,6 +98,10 @@ def test_problem(nx: int, ny: int, r: int, *, h: float | None = None,
     else:
         raise ValueError(init)
     b = source(xg[r:r + nx], yg[r:r + ny])
+    if rhs == "mehrstellen":
+        b = b + (h * h / 12.0) * source_laplacian(xg[r:r + nx], yg[r:r + ny])
+    elif rhs != "pointwise":
+        raise ValueError(rhs)
     return np.ascontiguousarray(u0), np.ascontiguousarray(b), h
 
 

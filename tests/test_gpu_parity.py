@@ -265,6 +265,46 @@ def test_too_deep_ring_is_invalid_arg():
     assert e.value.name == "CJM_ERR_INVALID_ARG"
 
 
+@pytest.mark.parametrize("kw", [dict(variant=7, warps=6), dict(variant=4, warps=5), dict(warps=-1),
+                                dict(variant=8), dict(variant=7, temporal_k=5),
+                                dict(variant=7, temporal_k=4, stages=2)])
+def test_invalid_launch_options_are_invalid_arg(kw):
+    with pytest.raises(cjm.CJMError) as e:
+        cjm.Plan(9, 256, 256, 1 / 257, 1e-8, **kw)
+    assert e.value.name == "CJM_ERR_INVALID_ARG"
+
+
+def test_17_point_k4_falls_back_to_the_shared_line_kernel():
+    r = 2
+    u0, b, h = inputs.test_problem(300, 200, r, init="random", seed=29)
+    with pytest.raises(cjm.CJMError):
+        cjm.Plan(17, 300, 200, h, 1e-8, temporal_k=4, variant=7)
+    with cjm.Plan(17, 300, 200, h, 1e-8, temporal_k=4) as plan:   # default variant: falls back
+        assert plan.info()["variant"] == 3 and plan.info()["temporal_k"] == 4
+        w = oracle_weights(17, 300, 200, plan)
+        ud = dev(u0)
+        plan.sweeps(dev(b), ud, 0, 9)
+    g = oracle.rhs_to_g(17, h, b)
+    want = oracle.sweeps(17, u0, g, w, 0, 9)
+    assert_field_parity(host(ud), want, r)
+
+
+def test_mehrstellen_rhs_solve_is_fourth_order_accurate():
+    """9-point solve with the Mehrstellen RHS (DESIGN R7) to tol 1e-12: the
+    oracle's field bitwise, and the real error at the direct solve's
+    fourth-order level (5.75e-11 at N = 128, SURVEY [V7])."""
+    n = 127
+    u0, b, h = inputs.test_problem(n, n, 1, rhs="mehrstellen")
+    uo, ro = oracle.solve(9, h, 1e-12, b, u0)
+    with cjm.Plan(9, n, n, h, 1e-12) as plan:
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud)
+    assert rep["status"] == "CJM_OK" and rep["iterations"] == ro["iterations"]
+    assert_field_parity(host(ud), uo, 1)
+    err = np.max(np.abs(host(ud)[1:-1, 1:-1] - inputs.exact_field(n, n, 1, h)))
+    assert err <= 1e-10
+
+
 def test_bad_pitch_is_invalid_arg():
     import ctypes as C
     u0, b, h = inputs.test_problem(64, 64, 1)

@@ -364,6 +364,36 @@ def test_discretisation_order(stencil, order):
     assert np.all(np.abs(slopes - order) < 0.15), slopes
 
 
+def test_source_laplacian_matches_finite_differences():
+    """The analytic Delta f used by the Mehrstellen RHS vs a fourth-order
+    finite-difference Laplacian of f itself (independent of the formula)."""
+    d = 1e-3
+    x = np.linspace(0.1, 0.9, 9)
+    X = np.arange(-2, 3) * d
+    for xi in x:
+        for yi in x:
+            f = inputs.source(xi + X, yi + X)             # 5 x 5 samples around (xi, yi)
+            c = np.array([-1, 16, -30, 16, -1]) / (12 * d * d)
+            lap = c @ f[2, :] + c @ f[:, 2]
+            want = inputs.source_laplacian(np.array([xi]), np.array([yi]))[0, 0]
+            assert lap == pytest.approx(want, rel=1e-7, abs=1e-8)
+
+
+def test_mehrstellen_rhs_makes_the_9_point_fourth_order():
+    """9-point alpha=2/3 with b = f + (h^2/12) Delta f (DESIGN R7): order 4
+    (SURVEY [V7]: 2.37e-7, 1.48e-8, 9.26e-10, 5.75e-11 at N = 16..128)."""
+    errs, hs = [], []
+    for N in (16, 32, 64, 128):
+        n = N - 1
+        u0, b, h = inputs.test_problem(n, n, 1, rhs="mehrstellen")
+        us = dense.direct_solve(9, u0, b, h)
+        errs.append(np.max(np.abs(us[1:1 + n, 1:1 + n] - inputs.exact_field(n, n, 1, h))))
+        hs.append(h)
+    slopes = np.diff(np.log(errs)) / np.diff(np.log(hs))
+    assert np.all(np.abs(slopes - 4.0) < 0.15), slopes
+    assert errs[2] == pytest.approx(9.26e-10, rel=0.03)
+
+
 def test_fig4_right_17pt_N128_reaches_1e8():
     """the 17-point stencil at N = 128 reaches real error 1e-8."""
     n = 127
