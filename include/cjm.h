@@ -228,6 +228,36 @@ cjm_status cjm_mask_set(cjm_plan_t p, const double *cW, const double *cE,
                         const double *cS, const double *cN, const double *cC,
                         long long ld_c, void *cuda_stream);
 
+/* Generic square masks (tab:ste1): "each of its
+ * (at most) 24 neighbors spanned by the discretization of the Laplacian can
+ * have different numerical factors ... [which] may change as a function of
+ * the position of the central node".  radius m = 1: (2m+1)^2 = 9-point masks
+ * (the upper, up-to-9-points data structure of tab:ste1); m = 2: 25-point
+ * masks (the most generic case, lower part of tab:ste1) -- e.g. the 9- and
+ * 17-point Laplacians of Eq. 9-points / Eq. 17-points with per-node factors.
+ *
+ * cjm_plan_mask_n: as cjm_plan_mask, with u holding m ghost rings
+ * ((ny+2m) x (nx+2m), ld_u >= nx + 2m; the outer ring is data too).
+ * Errors: INVALID_ARG (radius not 1 or 2, sizes, bounds, tol, options),
+ * UNSUPPORTED (world_size > 1), OOM, CUDA. */
+cjm_status cjm_plan_mask_n(cjm_plan_t *out, int nx, int ny, int radius, double kappa_min,
+                           double kappa_max, double tol, const cjm_options *opt);
+
+/* Upload the mask of a cjm_plan_mask_n plan: planes[q] for q = (dy+m)(2m+1)
+ * + (dx+m), dx, dy in -m..m, is a DEVICE array (ny x nx, pitch ld_c >= nx,
+ * PDE units) of the coefficient of neighbour (i+dx, j+dy) of node (i,j), or
+ * NULL when that neighbour is absent everywhere (it is then neither stored nor
+ * read nor added); planes[m(2m+1)+m] = c_C is required.  The plan stores
+ * a_q = -c_q / c_C and c_C.  One sweep (DESIGN R11):
+ *   J = fma(a_0, u_0, fma(a_1, u_1, ... fma(a_{Q-1}, u_{Q-1}, b/c_C)))
+ * over the present q (innermost = largest q), d = J - u_C,
+ * u' = fma(w, d, u_C); residual r = c_C d.  The planes array and the arrays
+ * it points to are read during the call only (it synchronises cuda_stream).
+ * Errors: INVALID_ARG (not a cjm_plan_mask_n plan, NULL planes or centre
+ * plane, ld_c < nx), CUDA. */
+cjm_status cjm_mask_set_n(cjm_plan_t p, const double *const *planes, long long ld_c,
+                          void *cuda_stream);
+
 /* Host-only estimate of the spectral bounds of D^-1 A for a 5-point mask
  * (the numeric fallback; HOST arrays laid out as in
  * cjm_mask_set).  The 5-point grid graph is bipartite, so the spectrum of

@@ -90,6 +90,14 @@ def lib():
         L.oracle_mask_solve.argtypes = [C.c_int, C.c_int, dp, dp, dp, dp, dp, C.c_long, dp, C.c_long,
                                         C.c_double, C.c_double, C.c_double, C.c_int, dp, C.c_long,
                                         C.POINTER(Report)]
+        pp = C.POINTER(C.c_void_p)
+        L.oracle_maskn_sweep.argtypes = [C.c_int, C.c_int, C.c_int, dp, C.c_long, pp, C.c_long, dp,
+                                         C.c_long, C.c_double, dp, C.c_long]
+        L.oracle_maskn_residual.argtypes = [C.c_int, C.c_int, C.c_int, dp, C.c_long, pp, C.c_long, dp,
+                                            C.c_long, dp, dp]
+        L.oracle_maskn_solve.argtypes = [C.c_int, C.c_int, C.c_int, pp, C.c_long, dp, C.c_long,
+                                         C.c_double, C.c_double, C.c_double, C.c_int, dp, C.c_long,
+                                         C.POINTER(Report)]
         L.oracle_num_threads.restype = C.c_int
         L.oracle_set_num_threads.argtypes = [C.c_int]
         _lib = L
@@ -257,6 +265,59 @@ def mask_solve(mask: dict, b: np.ndarray, u0: np.ndarray, kmin: float, kmax: flo
     rep = Report()
     lib().oracle_mask_solve(nx, ny, *ps, nx, _dp(b), nx, kmin, kmax, tol, max_cycles, _dp(u), u.shape[1],
                             C.byref(rep))
+    return u, rep.as_dict()
+
+
+def _maskn_args(planes):
+    """planes: list of (2m+1)^2 per-node coefficient arrays (ny x nx) or None."""
+    keep = [None if c is None else np.ascontiguousarray(c, dtype=np.float64) for c in planes]
+    arr = (C.c_void_p * len(keep))(*[None if c is None else c.ctypes.data for c in keep])
+    return keep, arr
+
+
+def maskn_radius(planes) -> int:
+    m = {9: 1, 25: 2}.get(len(planes))
+    if m is None:
+        raise ValueError("a generic mask has 9 (m = 1) or 25 (m = 2) planes")
+    return m
+
+
+def maskn_sweep(planes, u: np.ndarray, b: np.ndarray, w: float) -> np.ndarray:
+    """One weighted Jacobi sweep with a generic (2m+1)^2 mask (planes in
+    row-major mask order, q = (dy+m)(2m+1) + (dx+m); None = absent); u has m
+    ghost rings."""
+    m = maskn_radius(planes)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    ny, nx = b.shape
+    keep, arr = _maskn_args(planes)
+    out = u.copy()
+    lib().oracle_maskn_sweep(m, nx, ny, _dp(u), u.shape[1], arr, nx, _dp(b), nx, w, _dp(out), u.shape[1])
+    return out
+
+
+def maskn_residual(planes, u: np.ndarray, b: np.ndarray) -> tuple[float, float]:
+    m = maskn_radius(planes)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    ny, nx = b.shape
+    keep, arr = _maskn_args(planes)
+    l2, li = C.c_double(), C.c_double()
+    lib().oracle_maskn_residual(m, nx, ny, _dp(u), u.shape[1], arr, nx, _dp(b), nx, C.byref(l2),
+                                C.byref(li))
+    return l2.value, li.value
+
+
+def maskn_solve(planes, b: np.ndarray, u0: np.ndarray, kmin: float, kmax: float, tol: float,
+                max_cycles: int = 8):
+    m = maskn_radius(planes)
+    u = np.array(u0, dtype=np.float64, order="C", copy=True)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    ny, nx = b.shape
+    keep, arr = _maskn_args(planes)
+    rep = Report()
+    lib().oracle_maskn_solve(m, nx, ny, arr, nx, _dp(b), nx, kmin, kmax, tol, max_cycles, _dp(u),
+                             u.shape[1], C.byref(rep))
     return u, rep.as_dict()
 
 

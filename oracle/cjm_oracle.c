@@ -561,6 +561,133 @@ int oracle_mask_solve(int nx, int ny, const double *cW, const double *cE, const 
     return rep->status = status;
 }
 
+/* ---------------------------------------------------------------------------
+ * Generic (2m+1) x (2m+1) masks, m = 1 or 2 (NEXT-4, tab:ste1):
+ * "both the central node ... and each of its (at most) 24 neighbors spanned
+ * by the discretization of the Laplacian can have different numerical
+ * factors" which "may change as a function of the position of the central
+ * node".  m = 1 is the upper part of tab:ste1 (up to 9 points), m = 2 the
+ * most generic case (lower part, up to 25 points).  c[q] (q = (dy+m)(2m+1) +
+ * (dx+m), dx, dy in -m..m; x = first index, y = second) is the per-node
+ * coefficient of neighbour (i+dx, j+dy), row-major ny x nx with pitch ldc, or
+ * NULL for a neighbour that is absent everywhere; q_C = m(2m+1)+m is the
+ * centre.  u has m ghost rings: node (i,j) at u[(j-1+m) ldu + (i-1+m)].
+ * The Jacobi correction (DESIGN R11, one fixed association):
+ *   a_q = -c_q / c_C,  g = b / c_C,
+ *   J = fma(a_0, u_0, fma(a_1, u_1, ... fma(a_{Q-1}, u_{Q-1}, g)))  over the
+ *       present neighbours in increasing q (the innermost is the largest q),
+ *   d = J - uC,   u' = fma(w, d, uC),   r = c_C d.
+ * ------------------------------------------------------------------------- */
+static double maskn_d(int m, int i, int j, const double *u, long ldu, const double *const *c,
+                      long ldc, const double *b, long ldb, double *cc_out)
+{
+    int s = 2 * m + 1, qc = m * s + m;
+    long k = (long)(j - 1) * ldc + (i - 1);
+    double cc = c[qc][k];
+    double J = b[(long)(j - 1) * ldb + (i - 1)] / cc;
+    for (int q = s * s - 1; q >= 0; q--) {
+        if (q == qc || !c[q]) continue;
+        int dy = q / s - m, dx = q % s - m;
+        double a = -c[q][k] / cc;
+        J = fma(a, u[(long)(j - 1 + m + dy) * ldu + (i - 1 + m + dx)], J);
+    }
+    *cc_out = cc;
+    return J - u[(long)(j - 1 + m) * ldu + (i - 1 + m)];
+}
+
+void oracle_maskn_sweep(int m, int nx, int ny, const double *u, long ldu, const double *const *c,
+                        long ldc, const double *b, long ldb, double w, double *out, long ldo)
+{
+    #pragma omp parallel for schedule(static)
+    for (int j = 1; j <= ny; j++) {
+        for (int i = 1; i <= nx; i++) {
+            double cc;
+            double d = maskn_d(m, i, j, u, ldu, c, ldc, b, ldb, &cc);
+            double uc = u[(long)(j - 1 + m) * ldu + (i - 1 + m)];
+            out[(long)(j - 1 + m) * ldo + (i - 1 + m)] = fma(w, d, uc);
+        }
+    }
+}
+
+/* ||r||_2, ||r||_inf of r = c_C d; row sums in column order, rows in order. */
+void oracle_maskn_residual(int m, int nx, int ny, const double *u, long ldu,
+                           const double *const *c, long ldc, const double *b, long ldb,
+                           double *l2, double *linf)
+{
+    double *rs = (double *)malloc(sizeof(double) * (size_t)ny * 2);
+    #pragma omp parallel for schedule(static)
+    for (int j = 1; j <= ny; j++) {
+        double s = 0.0, mx = 0.0;
+        for (int i = 1; i <= nx; i++) {
+            double cc;
+            double d = maskn_d(m, i, j, u, ldu, c, ldc, b, ldb, &cc);
+            double r = cc * d;
+            s = s + r * r;
+            double ar = fabs(r);
+            if (ar > mx || ar != ar) mx = ar;
+        }
+        rs[2 * (j - 1)] = s;
+        rs[2 * (j - 1) + 1] = mx;
+    }
+    double s = 0.0, mx = 0.0;
+    for (int j = 0; j < ny; j++) {
+        s = s + rs[2 * j];
+        if (rs[2 * j + 1] > mx || rs[2 * j + 1] != rs[2 * j + 1]) mx = rs[2 * j + 1];
+    }
+    free(rs);
+    *l2 = sqrt(s);
+    *linf = mx;
+}
+
+/* The CJM with a generic (2m+1)^2 mask and caller-supplied spectral bounds. */
+int oracle_maskn_solve(int m, int nx, int ny, const double *const *c, long ldc, const double *b,
+                       long ldb, double kmin, double kmax, double tol, int max_cycles,
+                       double *u, long ldu, oracle_report *rep)
+{
+    memset(rep, 0, sizeof(*rep));
+    if (m < 1 || m > 2 || nx < 1 || ny < 1 || !(kmin > 0.0 && kmax > kmin) ||
+        !(tol > 0.0 && tol < 1.0))
+        return rep->status = OR_INVALID;
+    long mm = oracle_m_min(kmin, kmax, tol);
+    int a, bb;
+    long P = oracle_cycle_len(mm, &a, &bb);
+    rep->kappa_min = kmin; rep->kappa_max = kmax; rep->m_min = mm; rep->cycle_len = P;
+    long *t = (long *)malloc(sizeof(long) * (size_t)P);
+    double *w = (double *)malloc(sizeof(double) * (size_t)P);
+    oracle_ordering(a, bb, t);
+    oracle_weights(kmin, kmax, P, t, w);
+    free(t);
+    long rows = ny + 2 * m;
+    double *v = (double *)malloc(sizeof(double) * (size_t)rows * ldu);
+    memcpy(v, u, sizeof(double) * (size_t)rows * ldu);
+    double l2, li;
+    oracle_maskn_residual(m, nx, ny, u, ldu, c, ldc, b, ldb, &l2, &li);
+    rep->r0_l2 = rep->r_l2 = l2;
+    rep->r0_linf = rep->r_linf = li;
+    int status = OR_NOT_CONVERGED;
+    if (l2 == 0.0) status = OR_OK;
+    double *cur = u, *nxt = v;
+    double rho_prev = l2;
+    for (int cyc = 1; status == OR_NOT_CONVERGED && cyc <= max_cycles; cyc++) {
+        for (long k = 0; k < P; k++) {
+            oracle_maskn_sweep(m, nx, ny, cur, ldu, c, ldc, b, ldb, w[k], nxt, ldu);
+            double *tmp = cur; cur = nxt; nxt = tmp;
+        }
+        rep->iterations += P;
+        rep->cycles = cyc;
+        oracle_maskn_residual(m, nx, ny, cur, ldu, c, ldc, b, ldb, &l2, &li);
+        rep->r_l2 = l2;
+        rep->r_linf = li;
+        if (!isfinite(l2)) { status = OR_DIVERGED; break; }
+        if (l2 <= tol * rep->r0_l2) { status = OR_OK; break; }
+        if (l2 > 0.5 * rho_prev) { status = OR_STAGNATED; break; }
+        rho_prev = l2;
+    }
+    if (cur != u) memcpy(u, cur, sizeof(double) * (size_t)rows * ldu);
+    free(v); free(w);
+    return rep->status = status;
+}
+
 int oracle_num_threads(void)
 {
 #ifdef _OPENMP

@@ -37,7 +37,7 @@ EXPORTS = ("cjm_default_options", "cjm_schedule", "cjm_plan", "cjm_plan_info", "
            "cjm_solve_ref",
            "cjm_solve_host", "cjm_sweeps", "cjm_residual", "cjm_get_nccl_id", "cjm_slab", "cjm_halo_plan",
            "cjm_plan_destroy", "cjm_pool_trim", "cjm_status_str", "cjm_last_error", "cjm_version",
-           "cjm_plan_mask", "cjm_mask_set", "cjm_mask_bounds")
+           "cjm_plan_mask", "cjm_mask_set", "cjm_mask_bounds", "cjm_plan_mask_n", "cjm_mask_set_n")
 
 
 class CJMError(RuntimeError):
@@ -101,6 +101,9 @@ def lib():
     L.cjm_plan_mask.argtypes = [C.POINTER(vp), i, i, C.c_double, C.c_double, C.c_double,
                                 C.POINTER(Options)]
     L.cjm_mask_set.argtypes = [vp, vp, vp, vp, vp, vp, ll, vp]
+    L.cjm_plan_mask_n.argtypes = [C.POINTER(vp), i, i, i, C.c_double, C.c_double, C.c_double,
+                                  C.POINTER(Options)]
+    L.cjm_mask_set_n.argtypes = [vp, C.POINTER(vp), ll, vp]
     L.cjm_mask_bounds.argtypes = [i, i, vp, vp, vp, vp, vp, ll, i, dp, dp]
     L.cjm_plan_info.argtypes = [vp, C.POINTER(Report), C.POINTER(i), C.POINTER(i), C.POINTER(i),
                                 C.POINTER(dp)]
@@ -344,6 +347,50 @@ class MaskPlan(Plan):
         if len(lds) != 1:
             raise ValueError("mask arrays must share one pitch")
         _check(lib().cjm_mask_set(self._h, *ptrs, lds.pop(), _stream(stream)), "cjm_mask_set")
+
+
+class MaskPlanN(Plan):
+    """Owns a generic (2m+1)^2 mask plan (cjm_plan_mask_n ... cjm_plan_destroy),
+    m = radius 1 or 2.  `planes` (optional): list of (2m+1)^2 entries, each a
+    ny x nx float64 CUDA tensor or None (absent neighbour), in mask order
+    q = (dy+m)(2m+1) + (dx+m); passed to cjm_mask_set_n."""
+
+    def __init__(self, nx: int, ny: int, radius: int, kappa_min: float, kappa_max: float,
+                 tol: float, planes: list | None = None, **options):
+        self._h = C.c_void_p()
+        self._id_buf = None
+        o = cjm_default_options(**options)
+        _check(lib().cjm_plan_mask_n(C.byref(self._h), nx, ny, radius, kappa_min, kappa_max, tol,
+                                     C.byref(o)), "cjm_plan_mask_n")
+        self.stencil, self.nx, self.ny, self.h, self.tol = STENCIL_MASK, nx, ny, 1.0, tol
+        self.radius = radius
+        self._load_info()
+        if planes is not None:
+            self.mask_set(planes)
+
+    def mask_set(self, planes: list, stream=None) -> None:
+        q = (2 * self.radius + 1) ** 2
+        if len(planes) != q:
+            raise ValueError(f"a radius-{self.radius} mask has {q} planes, got {len(planes)}")
+        ptrs, lds = [], set()
+        for k, t in enumerate(planes):
+            if t is None:
+                ptrs.append(None)
+                continue
+            if tuple(t.shape) != (self.ny, self.nx):
+                raise ValueError(f"planes[{k}]: shape {tuple(t.shape)}, plan expects {(self.ny, self.nx)}")
+            p, ld = _dev_ptr(t, f"planes[{k}]")
+            ptrs.append(p)
+            lds.add(ld)
+        if len(lds) != 1:
+            raise ValueError("mask planes must share one pitch")
+        arr = (C.c_void_p * q)(*ptrs)
+        _check(lib().cjm_mask_set_n(self._h, arr, lds.pop(), _stream(stream)), "cjm_mask_set_n")
+
+
+def cjm_plan_mask_n(nx, ny, radius, kappa_min, kappa_max, tol=1e-8, planes=None,
+                    **options) -> MaskPlanN:
+    return MaskPlanN(nx, ny, radius, kappa_min, kappa_max, tol, planes=planes, **options)
 
 
 def cjm_plan_mask(nx, ny, kappa_min, kappa_max, tol=1e-8, mask=None, **options) -> MaskPlan:

@@ -193,6 +193,10 @@ struct cjm_plan_s {
   double* A = nullptr;
   size_t a_elems = 0;
   int mask_ready = 0, bands = 1;
+  int mask_r = 0;              // 0: 5-point cross (cjm_plan_mask); 1, 2: (2m+1)^2 masks
+  int nplanes = 5;             // coefficient planes stored (a_q ..., c_C)
+  int mask_qc = 4;             // plane holding c_C
+  unsigned int present = 0;    // square masks: neighbour planes present
   double* partials = nullptr;
   double* result = nullptr;
   double* result_host = nullptr;  // pinned, 2 doubles
@@ -264,13 +268,23 @@ int block_threads(const cjm_plan_s* pl) { return pl->variant >= 4 ? pl->nw * 32 
 // output rows [row0, row0 + nrows) of the slab (default: all of them).  Only
 // a launch with advance = 1 moves the device-side n / cur (the last launch of
 // a sweep that is split into bands).
+template <int MR>
+void launch_maskn(int mode, int grid, cudaStream_t st, const cjm::MaskParams& mp) {
+  switch (mode) {
+    case MODE_HOT: cjm::cjm_maskn_kernel<MR, false, true><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+    case MODE_CHECK: cjm::cjm_maskn_kernel<MR, true, true><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+    default: cjm::cjm_maskn_kernel<MR, true, false><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+  }
+}
+
 cjm_status launch_mask(cjm_plan_s* pl, int mode, cudaStream_t st) {
   cjm::MaskParams mp;
   mp.buf[0] = pl->buf[0];
   mp.buf[1] = pl->buf[1];
   mp.g = pl->G;
   mp.a = pl->A;
-  mp.plane = (long long)pl->a_elems / 5;
+  mp.plane = (long long)pl->a_elems / pl->nplanes;
+  mp.present = pl->present;
   mp.w = pl->w_dev;
   mp.state = pl->state;
   mp.partials = pl->partials;
@@ -282,10 +296,15 @@ cjm_status launch_mask(cjm_plan_s* pl, int mode, cudaStream_t st) {
   mp.bands = pl->bands;
   const long long strips = (pl->nx + cjm::MASK_NT - 1) / cjm::MASK_NT;
   const int grid = (int)std::min<long long>(pl->nctas, strips * pl->bands);
-  switch (mode) {
-    case MODE_HOT: cjm::cjm_mask_kernel<false, true><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
-    case MODE_CHECK: cjm::cjm_mask_kernel<true, true><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
-    default: cjm::cjm_mask_kernel<true, false><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+switch (pl->mask_r) {
+    case 1: launch_maskn<1>(mode, grid, st, mp); break;
+    case 2: launch_maskn<2>(mode, grid, st, mp); break;
+    default:
+      switch (mode) {
+        case MODE_HOT: cjm::cjm_mask_kernel<false, true><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+        case MODE_CHECK: cjm::cjm_mask_kernel<true, true><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+        default: cjm::cjm_mask_kernel<true, false><<<grid, cjm::MASK_NT, 0, st>>>(mp); break;
+      }
   }
   CUDA_TRY(cudaGetLastError());
   pl->launches += 1;
@@ -568,8 +587,8 @@ cjm_status stage_in(cjm_plan_s* pl, const double* rhs, long long ld_rhs, const d
     const long long total = (long long)pl->nx * grows;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
     if (pl->stencil == CJM_STENCIL_MASK)   // g = b / c_C
-      cjm::cjm_mask_scale_kernel<<<blocks, 256, 0, st>>>(g0, pl->ld, pl->nx, grows,
-                                                         pl->A + 4 * (pl->a_elems / 5));
+      cjm::cjm_mask_scale_kernel<<<blocks, 256, 0, st>>>(
+          g0, pl->ld, pl->nx, grows, pl->A + pl->mask_qc * (pl->a_elems / pl->nplanes));
     else
       cjm::cjm_scale_kernel<<<blocks, 256, 0, st>>>(g0, pl->ld, pl->nx, grows, pl->gscale);
     CUDA_TRY(cudaGetLastError());
@@ -845,7 +864,8 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
 
 // cjm_plan / cjm_plan_mask.  bounds = {kappa_min, kappa_max} for masks.
 static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, double h, int bc,
-                              double tol, const cjm_options* opt_in, const double* bounds) {
+                              double tol, const cjm_options* opt_in, const double* bounds,
+                              int mask_r = 0) {
   if (!out) return CJM_ERR_INVALID_ARG;
   *out = nullptr;
   const auto t0 = std::chrono::steady_clock::now();
@@ -861,7 +881,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     set_error("cjm_plan_mask", "generic-mask plans are single-GPU");
     return CJM_ERR_UNSUPPORTED;
   }
-  const int R = mask ? 1 : cjm::stencil_reach(stencil);
+  const int R = mask ? std::max(1, mask_r) : cjm::stencil_reach(stencil);
   if (!R || nx < 4 || ny < 4 || !(h > 0.0) || !std::isfinite(h) || !(tol > 0.0 && tol < 1.0) ||
       opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size ||
       (opt.world_size > 1 && !opt.nccl_id && !opt.external_halo) ||
@@ -1125,7 +1145,10 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   PLAN_CUDA(cudaMemset(pl->buf[1], 0, pl->buf_elems * sizeof(double)));
   PLAN_CUDA(cudaMemset(pl->G, 0, pl->g_elems * sizeof(double)));
   if (mask) {
-    pl->a_elems = 5 * (size_t)ny * pl->ld;
+    pl->mask_r = mask_r;
+    pl->nplanes = mask_r ? (2 * mask_r + 1) * (2 * mask_r + 1) : 5;
+    pl->mask_qc = mask_r ? mask_r * (2 * mask_r + 1) + mask_r : 4;
+    pl->a_elems = (size_t)pl->nplanes * ny * pl->ld;
     PLAN_CUDA(cjm::pool_alloc(dev, pl->a_elems * sizeof(double), (void**)&pl->A));
   }
   tt.mark("field buffers");
@@ -1215,18 +1238,59 @@ cjm_status cjm_plan_mask(cjm_plan_t* out, int nx, int ny, double kappa_min, doub
 
 cjm_status cjm_mask_set(cjm_plan_t p, const double* cW, const double* cE, const double* cS,
                         const double* cN, const double* cC, long long ld_c, void* cuda_stream) {
-  if (!p || p->stencil != CJM_STENCIL_MASK || !cW || !cE || !cS || !cN || !cC || ld_c < p->nx) {
-    set_error("cjm_mask_set", "invalid argument (not a mask plan, NULL array or ld_c < nx)");
+  if (!p || p->stencil != CJM_STENCIL_MASK || p->mask_r != 0 || !cW || !cE || !cS || !cN || !cC ||
+      ld_c < p->nx) {
+    set_error("cjm_mask_set", "invalid argument (not a 5-point mask plan, NULL array or ld_c < nx)");
     return CJM_ERR_INVALID_ARG;
   }
   CUDA_TRY(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const long long total = (long long)p->nx * p->ny;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-  cjm::cjm_mask_prepare_kernel<<<blocks, 256, 0, st>>>(p->A, (long long)p->a_elems / 5, p->ld, cW, cE,
-                                                       cS, cN, cC, ld_c, p->nx, p->ny);
+  cjm::cjm_mask_prepare_kernel<<<blocks, 256, 0, st>>>(p->A, (long long)p->a_elems / p->nplanes,
+                                                       p->ld, cW, cE, cS, cN, cC, ld_c, p->nx, p->ny);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
+  p->mask_ready = 1;
+  return CJM_OK;
+}
+
+cjm_status cjm_plan_mask_n(cjm_plan_t* out, int nx, int ny, int radius, double kappa_min,
+                           double kappa_max, double tol, const cjm_options* opt) {
+  if (!(kappa_min > 0.0 && kappa_max > kappa_min) || !std::isfinite(kappa_max) ||
+      (radius != 1 && radius != 2)) {
+    if (out) *out = nullptr;
+    set_error("cjm_plan_mask_n", "need radius 1 or 2 and 0 < kappa_min < kappa_max < inf");
+    return CJM_ERR_INVALID_ARG;
+  }
+  const double bounds[2] = {kappa_min, kappa_max};
+  return plan_create(out, CJM_STENCIL_MASK, nx, ny, 1.0, CJM_BC_DIRICHLET, tol, opt, bounds, radius);
+}
+
+cjm_status cjm_mask_set_n(cjm_plan_t p, const double* const* planes, long long ld_c,
+                          void* cuda_stream) {
+  if (!p || p->stencil != CJM_STENCIL_MASK || p->mask_r == 0 || !planes || ld_c < p->nx ||
+      !planes[p->mask_qc]) {
+    set_error("cjm_mask_set_n",
+              "invalid argument (not a square-mask plan, NULL planes / centre plane, ld_c < nx)");
+    return CJM_ERR_INVALID_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  cjm::MaskPlanes mp{};
+  unsigned int present = 0;
+  for (int q = 0; q < p->nplanes; ++q) {
+    mp.c[q] = planes[q];
+    if (planes[q] && q != p->mask_qc) present |= 1u << q;
+  }
+  const long long total = (long long)p->nx * p->ny;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  cjm::cjm_maskn_prepare_kernel<<<blocks, 256, 0, st>>>(p->A, (long long)p->a_elems / p->nplanes,
+                                                        p->ld, mp, p->nplanes, p->mask_qc, ld_c,
+                                                        p->nx, p->ny);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  p->present = present;
   p->mask_ready = 1;
   return CJM_OK;
 }

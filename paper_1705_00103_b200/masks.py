@@ -34,6 +34,49 @@ def _exact_xy(x, y):
     return -np.exp(x * y)
 
 
+# Fig. 1 / Eq. 9-points / Eq. 17-points as (2m+1) x (2m+1) coefficient masks
+# (PDE units x h^2): offsets (dx, dy) -> coefficient.
+_CART9 = {(0, 0): -20.0 / 6.0, (-1, 0): 4.0 / 6.0, (1, 0): 4.0 / 6.0, (0, -1): 4.0 / 6.0,
+          (0, 1): 4.0 / 6.0, (-1, -1): 1.0 / 6.0, (1, -1): 1.0 / 6.0, (-1, 1): 1.0 / 6.0,
+          (1, 1): 1.0 / 6.0}
+_CART17 = {(0, 0): -300.0 / 72.0}
+for _d, _c1, _c2 in ((1, 64.0, 16.0), (2, -4.0, -1.0)):
+    for _dx, _dy in ((-_d, 0), (_d, 0), (0, -_d), (0, _d)):
+        _CART17[(_dx, _dy)] = _c1 / 72.0
+    for _dx, _dy in ((-_d, -_d), (_d, -_d), (-_d, _d), (_d, _d)):
+        _CART17[(_dx, _dy)] = _c2 / 72.0
+
+
+def plane_index(m: int, dx: int, dy: int) -> int:
+    """Plane of neighbour (i+dx, j+dy) in a (2m+1)^2 mask (row-major, dy major)."""
+    return (dy + m) * (2 * m + 1) + (dx + m)
+
+
+def cartesian_n(stencil: int, nx: int, ny: int, h: float) -> list:
+    """The 9-point (m = 1) or 17-point (m = 2) Cartesian Laplacian (alpha =
+    2/3, Eq. 9-points / Eq. 17-points) as a generic mask of per-node planes
+    (tab:ste1: the most generic data structure); absent neighbours are None."""
+    table, m = {9: (_CART9, 1), 17: (_CART17, 2)}[stencil]
+    planes = [None] * (2 * m + 1) ** 2
+    for (dx, dy), c in table.items():
+        planes[plane_index(m, dx, dy)] = np.full((ny, nx), c / (h * h))
+    return planes
+
+
+def random_n(m: int, nx: int, ny: int, seed: int) -> list:
+    """A variable-coefficient (2m+1)^2 mask with every neighbour present:
+    neighbour coefficients in [0.1, 1), centre = -(sum of |neighbours|) x 1.25
+    (strictly diagonally dominant, so D^-1 A has a positive spectrum)."""
+    from . import inputs
+    q = (2 * m + 1) ** 2
+    planes = []
+    for k in range(q):
+        planes.append(0.55 + 0.45 * inputs.uniform_pm1(seed + k, nx * ny).reshape(ny, nx))
+    qc = plane_index(m, 0, 0)
+    planes[qc] = -1.25 * sum(planes[k] for k in range(q) if k != qc)
+    return planes
+
+
 def cartesian(nx: int, ny: int, h: float) -> dict:
     """tab:ste2 'Cartesian coordinates' with Dx = Dy = h (the 5-point stencil)."""
     one = np.full((ny, nx), 1.0 / (h * h))

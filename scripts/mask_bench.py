@@ -47,6 +47,27 @@ def sweeps(kind, n, count, **opts):
                 launches=rep["kernel_launches"])
 
 
+def sweeps_n(stencil, n, count):
+    """The Cartesian 9- / 17-point stencils as generic (2m+1)^2 masks: the
+    kernel streams the present planes + g + u and writes u'."""
+    m = 1 if stencil == 9 else 2
+    planes = masks.cartesian_n(stencil, n, n, 1.0 / (n + 1))
+    u0, b, h = inputs.test_problem(n, n, m)
+    ud, bd = torch.from_numpy(u0).cuda(), torch.from_numpy(b).cuda()
+    dp = [None if c is None else torch.from_numpy(c).cuda() for c in planes]
+    present = sum(c is not None for c in planes) - 1
+    bpl = 8.0 * (3 + present)
+    with cjm.MaskPlanN(n, n, m, 1e-6, 2.0 - 1e-6, 1e-8, planes=dp) as plan:
+        plan.sweeps(bd, ud, 0, min(count, 64))
+        rep = plan.sweeps(bd, ud, 0, count)
+    t = rep["sweep_s"] / max(rep["hot_launches"], 1)
+    peak, src = measured_peaks()
+    gbs = bpl * n * n / t / 1e9
+    return dict(kind=f"cartesian{stencil}_as_{2 * m + 1}x{2 * m + 1}_mask", n=n, sweeps=count,
+                bytes_per_lup=bpl, us_per_sweep=1e6 * t, glups=n * n / t / 1e9, algo_gbs=gbs,
+                peak_gbs=peak, peak_src=src, frac=gbs / peak)
+
+
 def solve(kind, n, tol=1e-8):
     mk, u0, b, ex = problem(kind, n)
     kmin, kmax = cjm.cjm_mask_bounds(mk, iters=2000)
@@ -68,9 +89,13 @@ if __name__ == "__main__":
     ap.add_argument("--count", type=int, default=400)
     ap.add_argument("--solve-n", type=int, default=1024)
     ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--square", action="store_true", help="also the (2m+1)^2 generic masks")
     a = ap.parse_args()
     for kind in ("polar", "bipolar", "cartesian"):
         print(json.dumps(sweeps(kind, a.n, a.count)), flush=True)
+    if a.square:
+        for st in (9, 17):
+            print(json.dumps(sweeps_n(st, a.n, a.count)), flush=True)
     if a.tune:
         for cps in (2, 3, 4, 5, 6, 8):
             print(json.dumps(sweeps("polar", a.n, a.count, ctas_per_sm=cps)), flush=True)

@@ -174,3 +174,108 @@ def test_mask_sweeps_bitwise_at_bench_size(kind):
     for k in range(3):
         want = oracle.mask_sweep(mk, want, b, float(w[(7 + k) % len(w)]))
     assert np.array_equal(got, want)
+
+
+# ----------------------------------------------- generic (2m+1)^2 masks (m = 1, 2)
+def dev_planes(planes):
+    return [None if c is None else torch.from_numpy(np.ascontiguousarray(c)).cuda() for c in planes]
+
+
+def _field(m, nx, ny, seed):
+    u = inputs.uniform_pm1(seed, (nx + 2 * m) * (ny + 2 * m)).reshape(ny + 2 * m, nx + 2 * m)
+    b = inputs.uniform_pm1(seed + 99, nx * ny).reshape(ny, nx)
+    return u, b
+
+
+KB = (1e-3, 1.9)   # bounds only enter through the weights (oracle_weights)
+
+
+@pytest.mark.parametrize("m", (1, 2))
+@pytest.mark.parametrize("nx,ny", [(4, 4), (37, 21), (300, 77), (257, 300), (520, 9)])
+@pytest.mark.parametrize("first,count", [(0, 1), (3, 5)])
+def test_maskn_sweeps_bitwise(m, nx, ny, first, count):
+    """Variable-coefficient (2m+1)^2 masks, every neighbour present: the
+    fields of cjm_sweeps equal the oracle's sweep by sweep (DESIGN R11)."""
+    planes = masks.random_n(m, nx, ny, seed=nx + 3 * ny + m)
+    u, b = _field(m, nx, ny, 5 + nx)
+    _, w = oracle_weights(*KB, 1e-8)
+    with cjm.MaskPlanN(nx, ny, m, *KB, 1e-8, planes=dev_planes(planes)) as plan:
+        assert np.array_equal(plan.info()["weights"], w)
+        ud = torch.from_numpy(u.copy()).cuda()
+        plan.sweeps(torch.from_numpy(b).cuda(), ud, first, count)
+        got = ud.cpu().numpy()
+    want = u.copy()
+    for k in range(count):
+        want = oracle.maskn_sweep(planes, want, b, float(w[(first + k) % len(w)]))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("stencil", (9, 17))
+def test_maskn_absent_planes_bitwise(stencil):
+    """The Cartesian 9- / 17-point Laplacians as masks (absent neighbours are
+    neither read nor added)."""
+    m = 1 if stencil == 9 else 2
+    nx, ny = 301, 157
+    u0, b, h = inputs.test_problem(nx, ny, m, init="random", seed=9)
+    planes = masks.cartesian_n(stencil, nx, ny, h)
+    _, w = oracle_weights(*KB, 1e-8)
+    with cjm.MaskPlanN(nx, ny, m, *KB, 1e-8, planes=dev_planes(planes)) as plan:
+        ud = torch.from_numpy(u0.copy()).cuda()
+        plan.sweeps(torch.from_numpy(b).cuda(), ud, 1, 4)
+        got = ud.cpu().numpy()
+        l2, li = plan.residual(torch.from_numpy(b).cuda(), torch.from_numpy(u0).cuda())
+    want = u0.copy()
+    for k in range(4):
+        want = oracle.maskn_sweep(planes, want, b, float(w[(1 + k) % len(w)]))
+    assert np.array_equal(got, want)
+    ol2, oli = oracle.maskn_residual(planes, u0, b)
+    assert l2 == pytest.approx(ol2, rel=1e-12) and li == oli
+
+
+@pytest.mark.parametrize("stencil", (9, 17))
+def test_maskn_cartesian_solve_matches_oracle(stencil):
+    """Solve to tol with the Cartesian stencils given as generic masks and the
+    closed-form bounds: same iterations, bitwise field as the oracle's."""
+    m = 1 if stencil == 9 else 2
+    n = 95
+    u0, b, h = inputs.test_problem(n, n, m)
+    kmin, kmax = oracle.bounds(stencil, n, n)
+    planes = masks.cartesian_n(stencil, n, n, h)
+    uo, ro = oracle.maskn_solve(planes, b, u0, kmin, kmax, 1e-8)
+    with cjm.MaskPlanN(n, n, m, kmin, kmax, 1e-8, planes=dev_planes(planes)) as plan:
+        ud = torch.from_numpy(u0.copy()).cuda()
+        rep = plan.solve(torch.from_numpy(b).cuda(), ud)
+    assert rep["status"] == "CJM_OK" and ro["status"] == "OK"
+    assert rep["iterations"] == ro["iterations"]
+    assert rep["r_l2"] == pytest.approx(ro["r_l2"], rel=1e-9)
+    assert np.array_equal(ud.cpu().numpy(), uo)
+
+
+def test_maskn_invalid_arguments():
+    with pytest.raises(cjm.CJMError):
+        cjm.MaskPlanN(32, 32, 3, *KB, 1e-8)
+    planes = masks.cartesian_n(9, 32, 32, 1 / 33)
+    planes[4] = None                                   # the centre plane is required
+    with cjm.MaskPlanN(32, 32, 1, *KB, 1e-8) as plan:
+        with pytest.raises(cjm.CJMError):
+            plan.mask_set(dev_planes(planes))
+        with pytest.raises(cjm.CJMError):              # mask_set first
+            plan.sweeps(torch.zeros(32, 32, dtype=torch.float64, device="cuda"),
+                        torch.zeros(34, 34, dtype=torch.float64, device="cuda"), 0, 1)
+
+
+@pytest.mark.parametrize("m", (1, 2))
+def test_maskn_sweeps_bitwise_at_bench_size(m):
+    n = 4096
+    planes = masks.cartesian_n(9 if m == 1 else 17, n, n, 1 / (n + 1))
+    u = inputs.uniform_pm1(3, (n + 2 * m) ** 2).reshape(n + 2 * m, n + 2 * m)
+    b = inputs.uniform_pm1(4, n * n).reshape(n, n)
+    _, w = oracle_weights(*KB, 1e-8)
+    with cjm.MaskPlanN(n, n, m, *KB, 1e-8, planes=dev_planes(planes)) as plan:
+        ud = torch.from_numpy(u.copy()).cuda()
+        plan.sweeps(torch.from_numpy(b).cuda(), ud, 7, 3)
+        got = ud.cpu().numpy()
+    want = u
+    for k in range(3):
+        want = oracle.maskn_sweep(planes, want, b, float(w[(7 + k) % len(w)]))
+    assert np.array_equal(got, want)

@@ -135,3 +135,103 @@ def test_bipolar_printed_single_power_factor_is_not_the_laplacian():
         us = spla.spsolve(A.tocsc(), b.ravel() - G @ u0.ravel()).reshape(n, n)
         errs.append(np.max(np.abs(us - ex)))
     assert min(errs) > 1e-2                               # O(1): not a consistent Laplacian
+
+
+# ----------------------------------------------- generic (2m+1)^2 masks (m = 1, 2)
+def assemble_n(planes):
+    """Sparse A (interior) and ghost coupling of a per-node (2m+1)^2 mask."""
+    m = oracle.maskn_radius(planes)
+    s = 2 * m + 1
+    ny, nx = planes[m * s + m].shape
+    W = nx + 2 * m
+    rows, cols, vals, g_rows, g_cols, g_vals = [], [], [], [], [], []
+    for j in range(ny):
+        for i in range(nx):
+            k = j * nx + i
+            for q, c in enumerate(planes):
+                if c is None:
+                    continue
+                dy, dx = q // s - m, q % s - m
+                p, r = i + dx, j + dy
+                if 0 <= p < nx and 0 <= r < ny:
+                    rows.append(k); cols.append(r * nx + p); vals.append(c[j, i])
+                else:
+                    g_rows.append(k); g_cols.append((r + m) * W + (p + m)); g_vals.append(c[j, i])
+    A = sp.csr_matrix((vals, (rows, cols)), shape=(nx * ny, nx * ny))
+    G = sp.csr_matrix((g_vals, (g_rows, g_cols)), shape=(nx * ny, (ny + 2 * m) * W))
+    return A, G
+
+
+def _random_field(m, nx, ny, seed):
+    u = inputs.uniform_pm1(seed, (nx + 2 * m) * (ny + 2 * m)).reshape(ny + 2 * m, nx + 2 * m)
+    b = inputs.uniform_pm1(seed + 99, nx * ny).reshape(ny, nx)
+    return u, b
+
+
+@pytest.mark.parametrize("m,nx,ny", [(1, 7, 5), (1, 12, 9), (2, 7, 6), (2, 11, 13)])
+def test_maskn_sweep_and_residual_match_dense(m, nx, ny):
+    """u' = u + w D^-1 (b - A u) and r = b - A u with A assembled from the
+    planes (every neighbour with its own per-node factor)."""
+    planes = masks.random_n(m, nx, ny, seed=5 + m)
+    u, b = _random_field(m, nx, ny, 41)
+    A, G = assemble_n(planes)
+    inner = u[m:m + ny, m:m + nx].ravel()
+    r = b.ravel() - (A @ inner + G @ u.ravel())
+    cc = planes[m * (2 * m + 1) + m].ravel()
+    w = 0.37
+    got = oracle.maskn_sweep(planes, u, b, w)
+    want = inner + w * r / cc
+    assert np.allclose(got[m:m + ny, m:m + nx].ravel(), want, rtol=1e-13, atol=1e-13)
+    assert np.array_equal(got[:m], u[:m]) and np.array_equal(got[:, :m], u[:, :m])
+    l2, li = oracle.maskn_residual(planes, u, b)
+    assert l2 == pytest.approx(np.linalg.norm(r), rel=1e-12)
+    assert li == pytest.approx(np.max(np.abs(r)), rel=1e-12)
+
+
+@pytest.mark.parametrize("stencil", (9, 17))
+def test_maskn_cartesian_is_the_builtin_stencil(stencil):
+    """The 9- / 17-point Laplacians as generic masks sweep like the built-in
+    stencils (Eq. 9-points, Eq. 17-points), up to the association."""
+    m = 1 if stencil == 9 else 2
+    n = 23
+    u0, b, h = inputs.test_problem(n, n, m, init="random", seed=3)
+    planes = masks.cartesian_n(stencil, n, n, h)
+    w = 1.3
+    got = oracle.maskn_sweep(planes, u0, b, w)
+    want = oracle.sweep(stencil, u0, oracle.rhs_to_g(stencil, h, b), w)
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("stencil,err", [(9, 1.40e-5), (17, 3.68e-9)])
+def test_maskn_cartesian_solve_reaches_the_discretisation_error(stencil, err):
+    """CJM with the Cartesian stencils given as generic masks and the closed-
+    form bounds: converges and its real error is the direct solve's (SURVEY
+    [V7] at N = 64)."""
+    m = 1 if stencil == 9 else 2
+    n = 63
+    u0, b, h = inputs.test_problem(n, n, m)
+    kmin, kmax = oracle.bounds(stencil, n, n)
+    planes = masks.cartesian_n(stencil, n, n, h)
+    u, rep = oracle.maskn_solve(planes, b, u0, kmin, kmax, 1e-12)
+    assert rep["status"] == "OK"
+    e = np.max(np.abs(u[m:-m, m:-m] - inputs.exact_field(n, n, m, h)))
+    assert e == pytest.approx(err, rel=0.05)
+
+
+@pytest.mark.parametrize("m", (1, 2))
+def test_maskn_solve_variable_coefficients_reaches_direct_solution(m):
+    """A variable-coefficient mask with dense spectral bounds: the CJM
+    converges in one cycle to the sparse direct solution."""
+    nx, ny = 13, 11
+    planes = masks.random_n(m, nx, ny, seed=2 + m)
+    u0, b = _random_field(m, nx, ny, 7)
+    u0[m:m + ny, m:m + nx] = 0.0
+    A, G = assemble_n(planes)
+    cc = planes[m * (2 * m + 1) + m].ravel()
+    ev = np.linalg.eigvals((A.toarray().T / cc).T)
+    kmin, kmax = float(np.min(ev.real)), float(np.max(ev.real))
+    assert kmin > 0
+    ustar = spla.spsolve(A.tocsc(), b.ravel() - G @ u0.ravel())
+    u, rep = oracle.maskn_solve(planes, b, u0, kmin * (1 - 1e-9), kmax * (1 + 1e-9), 1e-10)
+    assert rep["status"] == "OK"
+    assert np.max(np.abs(u[m:m + ny, m:m + nx].ravel() - ustar)) <= 1e-8 * np.max(np.abs(ustar))
