@@ -1015,9 +1015,12 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   // resident).  Check / residual / remainder kernels may need more registers;
   // they then run the same grid in more than one wave, which is correct
   // because no CTA ever waits for another.
-  if ((opt.warps != 0 && (pl->variant != 7 || (opt.warps != 4 && opt.warps != 5 && opt.warps != 7))) ||
+  if ((opt.warps != 0 &&
+       (pl->variant != 7 ||
+        (opt.warps != 4 && opt.warps != 5 && opt.warps != 7 &&
+         !(opt.warps == 11 && R == 1 && pl->K == 4)))) ||
       opt.warps < 0) {
-    set_error("cjm_plan", "warps must be 4, 5 or 7, with variant 7");
+    set_error("cjm_plan", "warps must be 4, 5 or 7 (or 11 for the 5/9-point at K = 4), with variant 7");
     return fail(CJM_ERR_INVALID_ARG);
   }
   if (pl->variant == 7) {
@@ -1025,18 +1028,23 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     // consumer warps resident per SM (registers are split between the SM's
     // 4 sub-partitions, shared memory holds stages x (2r+1) rows per CTA);
     // ties: the deeper ring, then fewer warps.
-    const int nws[3] = {4, 5, 7};
+    // (11 warps: one CTA per SM, 5/9-point at K = 4 only -- 23.7 vs 24.0 us
+    // per sweep at 4096^2, 328 vs 346 at 16384^2, profiles/r01_v7_tune.jsonl)
+    const int nws[4] = {4, 5, 7, 11};
+    constexpr int NNW = 4;
     const int st_hi = opt.stages > 0 ? opt.stages : (R == 1 ? 6 : 4);
     const int st_lo = opt.stages > 0 ? opt.stages : 4;
     int best = -1, best_nw = 4, best_st = st_hi;
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < NNW; ++i) {
       if (opt.warps && nws[i] != opt.warps) continue;
+      if (nws[i] == 11 && !(R == 1 && pl->K == 4)) continue;
       for (int stg = st_hi; stg >= st_lo; --stg) {
         pl->nw = nws[i];
         pl->stages = stg;
         const size_t sm = smem_bytes(pl, pl->K);
         if (sm > (size_t)smem_optin - 2048) continue;
         KernelFn k = pick_kernel(stencil, 7, pl->NT, pl->K, MODE_HOT, pl->nw);
+        if (!k) continue;                       // (nw, K) not instantiated
         PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sm));
         int occ = 0;

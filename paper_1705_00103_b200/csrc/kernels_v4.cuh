@@ -58,6 +58,11 @@ KernelFn pick_variant_v4(int variant, int K, int mode, int nw) {
     default: break;
   }
 #endif
+  if constexpr (Point<ST>::R == 1) {   // one CTA of 11 consumer warps per SM (K = 4)
+    if (nw == 11)   // K = 4, and K = 1 for remainder sweeps and residuals
+      return K == 4 ? pick_mode_v4<ST, 4, 2, RPS, 11>(mode)
+           : K == 1 ? pick_mode_v4<ST, 1, 2, RPS, 11>(mode) : nullptr;
+  }
   return nw == 5 ? pick_k_v4<ST, 2, RPS, 5>(K, mode)
        : nw == 7 ? pick_k_v4<ST, 2, RPS, 7>(K, mode) : pick_k_v4<ST, 2, RPS, 4>(K, mode);
 }

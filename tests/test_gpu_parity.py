@@ -149,6 +149,8 @@ def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows, dyn_pct, mo
                                  dict(variant=7, warps=7, temporal_k=2, stages=3),
                                  dict(variant=7, warps=4, temporal_k=3, stages=5, ctas_per_sm=1),
                                  dict(variant=7, temporal_k=4, chunk_rows=24),
+                                 dict(variant=7, temporal_k=4, warps=11),
+                                 dict(variant=7, temporal_k=4, warps=11, stages=4, chunk_rows=5),
                                  dict(variant=7, temporal_k=3, chunk_rows=-1),
                                  dict(variant=4, temporal_k=2, chunk_rows=100, ctas_per_sm=1)])
 def test_launch_configuration_does_not_change_result(cfg):
@@ -266,6 +268,7 @@ def test_too_deep_ring_is_invalid_arg():
 
 
 @pytest.mark.parametrize("kw", [dict(variant=7, warps=6), dict(variant=4, warps=5), dict(warps=-1),
+                                dict(variant=7, temporal_k=3, warps=11),
                                 dict(variant=8), dict(variant=7, temporal_k=5),
                                 dict(variant=7, temporal_k=4, stages=2)])
 def test_invalid_launch_options_are_invalid_arg(kw):
