@@ -340,7 +340,10 @@ def main():
                          # (24 B per lattice update): > 1 because a
                          # launch moves 24 B per node for K updates
                          "lup_roofline_frac": K * float(nx) * nyl / t_launch * BYTES_PER_LUP
-                                              / 1e9 / peak},
+                                              / 1e9 / peak,
+                         "note": (f"{K} sweeps per launch share one pass over HBM (24 B per node "
+                                  "per launch); with K > 1 the launch is fp64-latency bound, not "
+                                  "HBM bound (DESIGN section 5)") if K > 1 else None},
             "breakdown_ms": {"plan": 1e3 * statistics.mean(r["plan_s"] for r in reps),
                              "solve_device": 1e3 * statistics.mean(r["solve_s"] for r in reps),
                              "hot_sweeps": 1e3 * statistics.mean(r["sweep_s"] for r in reps)},
