@@ -284,7 +284,6 @@ __device__ __forceinline__ void consumer_segment(ConsumerState<Point<STENCIL>::R
   constexpr int E = TileGeom<R, K>::E;
   constexpr int ROW = T + 8;
   const long long ld = p.ld;
-  const int rows = p.rows;
       const int ca = c0 + 2 * tid, cb = ca + 1;
       const bool ina = ca >= 0 && ca < p.nx, inb = cb >= 0 && cb < p.nx;
       const bool owna = ina && ca >= c0 + E && ca < c0 + T - E;
