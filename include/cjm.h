@@ -258,6 +258,20 @@ cjm_status cjm_plan_mask_n(cjm_plan_t *out, int nx, int ny, int radius, double k
 cjm_status cjm_mask_set_n(cjm_plan_t p, const double *const *planes, long long ld_c,
                           void *cuda_stream);
 
+/* Host-only estimate of the spectral bounds of D^-1 A for a (2m+1)^2 mask
+ * (SURVEY A14's numeric fallback; HOST planes laid out as in cjm_mask_set_n,
+ * NULL = absent).  No symmetry to exploit: kappa_max by `iters` power-
+ * iteration steps on D^-1 A (0 = 2000), kappa_min by as many on
+ * kappa_max I - D^-1 A, both from sin(pi i/(nx+1)) sin(pi j/(ny+1)).  An
+ * estimate for a symmetrisable D^-1 A: both ends are approached from inside
+ * the spectrum, and the kappa_min estimate needs iterations ~ kappa_max /
+ * (gap at the bottom of the spectrum) -- fine on coarse grids, not on 4096^2
+ * (pass closed-form or safety-widened bounds there).  Cost 2 x iters x nx x
+ * ny x (2m+1)^2 on one host core.  Errors: INVALID_ARG (radius, sizes, NULL
+ * centre plane, a zero or non-finite c_C, an estimate kappa_min <= 0). */
+cjm_status cjm_mask_bounds_n(int nx, int ny, int radius, const double *const *planes,
+                             long long ld_c, int iters, double *kappa_min, double *kappa_max);
+
 /* Host-only estimate of the spectral bounds of D^-1 A for a 5-point mask
  * (the numeric fallback; HOST arrays laid out as in
  * cjm_mask_set).  The 5-point grid graph is bipartite, so the spectrum of

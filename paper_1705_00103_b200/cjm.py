@@ -37,7 +37,8 @@ EXPORTS = ("cjm_default_options", "cjm_schedule", "cjm_plan", "cjm_plan_info", "
            "cjm_solve_ref",
            "cjm_solve_host", "cjm_sweeps", "cjm_residual", "cjm_get_nccl_id", "cjm_slab", "cjm_halo_plan",
            "cjm_plan_destroy", "cjm_pool_trim", "cjm_status_str", "cjm_last_error", "cjm_version",
-           "cjm_plan_mask", "cjm_mask_set", "cjm_mask_bounds", "cjm_plan_mask_n", "cjm_mask_set_n")
+           "cjm_plan_mask", "cjm_mask_set", "cjm_mask_bounds", "cjm_plan_mask_n", "cjm_mask_set_n",
+           "cjm_mask_bounds_n")
 
 
 class CJMError(RuntimeError):
@@ -104,6 +105,7 @@ def lib():
     L.cjm_plan_mask_n.argtypes = [C.POINTER(vp), i, i, i, C.c_double, C.c_double, C.c_double,
                                   C.POINTER(Options)]
     L.cjm_mask_set_n.argtypes = [vp, C.POINTER(vp), ll, vp]
+    L.cjm_mask_bounds_n.argtypes = [i, i, i, C.POINTER(vp), ll, i, dp, dp]
     L.cjm_mask_bounds.argtypes = [i, i, vp, vp, vp, vp, vp, ll, i, dp, dp]
     L.cjm_plan_info.argtypes = [vp, C.POINTER(Report), C.POINTER(i), C.POINTER(i), C.POINTER(i),
                                 C.POINTER(dp)]
@@ -411,6 +413,22 @@ def cjm_mask_bounds(mask: dict, iters: int = 0) -> tuple[float, float]:
     kmin, kmax = C.c_double(), C.c_double()
     _check(lib().cjm_mask_bounds(nx, ny, *[C.c_void_p(a.ctypes.data) for a in arrs], nx, iters,
                                  C.byref(kmin), C.byref(kmax)), "cjm_mask_bounds")
+    return kmin.value, kmax.value
+
+
+def cjm_mask_bounds_n(planes: list, iters: int = 0) -> tuple[float, float]:
+    """Host estimate (kappa_min, kappa_max) of D^-1 A for a (2m+1)^2 mask of
+    host float64 planes (None = absent), cjm_mask_bounds_n."""
+    q = len(planes)
+    m = {9: 1, 25: 2}.get(q)
+    if m is None:
+        raise ValueError("a square mask has 9 or 25 planes")
+    arrs = [None if c is None else np.ascontiguousarray(c, dtype=np.float64) for c in planes]
+    ny, nx = arrs[m * (2 * m + 1) + m].shape
+    ptrs = (C.c_void_p * q)(*[None if a is None else a.ctypes.data for a in arrs])
+    kmin, kmax = C.c_double(), C.c_double()
+    _check(lib().cjm_mask_bounds_n(nx, ny, m, ptrs, nx, iters, C.byref(kmin), C.byref(kmax)),
+           "cjm_mask_bounds_n")
     return kmin.value, kmax.value
 
 

@@ -1318,6 +1318,21 @@ cjm_status cjm_mask_bounds(int nx, int ny, const double* cW, const double* cE, c
   return CJM_OK;
 }
 
+cjm_status cjm_mask_bounds_n(int nx, int ny, int radius, const double* const* planes, long long ld_c,
+                             int iters, double* kappa_min, double* kappa_max) {
+  double kmin = 0, kmax = 0;
+  if (!kappa_min || !kappa_max ||
+      !cjm::mask_spectral_bounds_n(radius, nx, ny, planes, ld_c, iters > 0 ? iters : 2000, &kmin,
+                                   &kmax)) {
+    set_error("cjm_mask_bounds_n",
+              "invalid argument, zero / non-finite c_C or D^-1 A not positive definite");
+    return CJM_ERR_INVALID_ARG;
+  }
+  *kappa_min = kmin;
+  *kappa_max = kmax;
+  return CJM_OK;
+}
+
 cjm_status cjm_plan_info(cjm_plan_t p, cjm_report* info, int* reach, int* y0, int* ny_local,
                          const double** host_weights) {
   if (!p) return CJM_ERR_INVALID_ARG;

@@ -32,6 +32,9 @@ bool build_schedule_bounds(double kmin, double kmax, double tol, int order, Sche
 bool mask_spectral_bounds(int nx, int ny, const double* cW, const double* cE, const double* cS,
                           const double* cN, const double* cC, long long ldc, int iters,
                           double* kmin, double* kmax);
+// the same for a (2m+1)^2 mask (both ends by power iteration)
+bool mask_spectral_bounds_n(int m, int nx, int ny, const double* const* c, long long ldc, int iters,
+                            double* kmin, double* kmax);
 
 // device-buffer cache (pool.cpp)
 cudaError_t pool_alloc(int device, size_t bytes, void** out);

@@ -75,4 +75,71 @@ bool mask_spectral_bounds(int nx, int ny, const double* cW, const double* cE, co
   return true;
 }
 
+// Square (2m+1)^2 masks (cjm_mask_bounds_n): no bipartite symmetry, so both
+// ends are estimated.  B = D^-1 A, (B x)_k = x_k - sum_q a_q x_{k+q} over the
+// interior neighbours (a_q = -c_q / c_C).  kappa_max: power iteration on B
+// (the norm ratio ||B x|| / ||x||, from below for a symmetrisable B);
+// kappa_min: power iteration on sigma I - B with sigma = kappa_max (its
+// dominant eigenvalue is sigma - kappa_min).  Both start from the smooth
+// positive vector; cost 2 x iters x nx x ny x (2m+1)^2 on one host core.
+bool mask_spectral_bounds_n(int m, int nx, int ny, const double* const* c, long long ldc,
+                            int iters, double* kmin, double* kmax) {
+  if (m < 1 || m > 2 || nx < 1 || ny < 1 || ldc < nx || !c || iters < 1) return false;
+  const int S = 2 * m + 1, QC = m * S + m;
+  if (!c[QC]) return false;
+  const size_t n = (size_t)nx * ny;
+  std::vector<double> x0(n), x(n), y(n);
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      const double cc = c[QC][(long long)j * ldc + i];
+      if (!(cc != 0.0) || !std::isfinite(cc)) return false;
+      x0[(size_t)j * nx + i] =
+          std::sin(M_PI * (i + 1) / (nx + 1.0)) * std::sin(M_PI * (j + 1) / (ny + 1.0));
+    }
+  // out = shift * in - B in
+  auto apply = [&](double shift, const std::vector<double>& in, std::vector<double>& out) {
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        const long long k = (long long)j * ldc + i;
+        const size_t e = (size_t)j * nx + i;
+        const double cc = c[QC][k];
+        double s = 0.0;
+        for (int q = 0; q < S * S; ++q) {
+          if (q == QC || !c[q]) continue;
+          const int ii = i + q % S - m, jj = j + q / S - m;
+          if (ii < 0 || ii >= nx || jj < 0 || jj >= ny) continue;   // Dirichlet ghost
+          s += (-c[q][k] / cc) * in[(size_t)jj * nx + ii];
+        }
+        out[e] = shift * in[e] - (in[e] - s);
+      }
+  };
+  auto norm = [](const std::vector<double>& v) {
+    double s = 0.0;
+    for (double q : v) s += q * q;
+    return std::sqrt(s);
+  };
+  auto power = [&](double shift, double sign, double* lam) {
+    x = x0;
+    double nrm = norm(x);
+    for (int it = 0; it < iters; ++it) {
+      for (double& q : x) q /= nrm;
+      apply(shift, x, y);
+      for (double& q : y) q *= sign;
+      nrm = norm(y);
+      if (!(nrm > 0.0) || !std::isfinite(nrm)) return false;
+      x.swap(y);
+    }
+    *lam = nrm;
+    return true;
+  };
+  double lmax = 0.0, mu = 0.0;
+  if (!power(0.0, -1.0, &lmax)) return false;          // ||B x||: 0 I - B, sign flipped
+  if (!power(lmax, 1.0, &mu)) return false;             // ||(lmax I - B) x||
+  const double lmin = lmax - mu;
+  if (!(lmin > 0.0) || !(lmax > lmin)) return false;    // not positive definite: CJM does not apply
+  *kmin = lmin;
+  *kmax = lmax;
+  return true;
+}
+
 }  // namespace cjm

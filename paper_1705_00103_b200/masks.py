@@ -77,6 +77,34 @@ def random_n(m: int, nx: int, ny: int, seed: int) -> list:
     return planes
 
 
+def symmetric_n(m: int, nx: int, ny: int, seed: int) -> list:
+    """A variable-coefficient (2m+1)^2 mask whose operator is symmetric: every
+    edge (node, node + (dx, dy)) gets one weight in [0.1, 1) used by both of
+    its nodes, centre = -1.25 x the node's weight sum (so D^-1 A is similar
+    to a symmetric positive definite matrix: real, positive spectrum)."""
+    from . import inputs
+    s = 2 * m + 1
+    planes = [None] * (s * s)
+    qc = plane_index(m, 0, 0)
+    total = np.zeros((ny, nx))
+    k = 0
+    for dy in range(-m, m + 1):
+        for dx in range(-m, m + 1):
+            if (dy, dx) <= (0, 0):
+                continue                      # each undirected edge once: (dx, dy) > 0
+            wgt = 0.55 + 0.45 * inputs.uniform_pm1(seed + k, (ny + 2 * m) * (nx + 2 * m)) \
+                .reshape(ny + 2 * m, nx + 2 * m)
+            k += 1
+            # edge weight stored at the lower endpoint (i, j) of (i, j) -- (i+dx, j+dy)
+            fwd = wgt[m:m + ny, m:m + nx]
+            bwd = wgt[m - dy:m - dy + ny, m - dx:m - dx + nx]
+            planes[plane_index(m, dx, dy)] = fwd.copy()
+            planes[plane_index(m, -dx, -dy)] = bwd.copy()
+            total += fwd + bwd
+    planes[qc] = -1.25 * total
+    return planes
+
+
 def cartesian(nx: int, ny: int, h: float) -> dict:
     """tab:ste2 'Cartesian coordinates' with Dx = Dy = h (the 5-point stencil)."""
     one = np.full((ny, nx), 1.0 / (h * h))

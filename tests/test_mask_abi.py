@@ -62,3 +62,37 @@ def test_plan_mask_rejects_bad_arguments_before_touching_the_device():
         cjm.Plan(cjm.STENCIL_MASK, 64, 64, 0.1, 1e-8)
     assert e.value.name == "CJM_ERR_INVALID_ARG"
 
+
+
+@pytest.mark.parametrize("m,nx,ny", [(1, 12, 10), (2, 11, 13)])
+@pytest.mark.parametrize("kind", ("cartesian", "symmetric"))
+def test_mask_bounds_n_match_dense_eigenvalues(m, nx, ny, kind):
+    """cjm_mask_bounds_n (host power iterations, no GPU) vs the dense spectrum
+    of D^-1 A for square masks (SURVEY A14's numeric fallback)."""
+    import numpy as np
+    from paper_1705_00103_b200 import masks
+    if kind == "cartesian":
+        planes = masks.cartesian_n(9 if m == 1 else 17, nx, ny, 1.0 / (nx + 1))
+    else:
+        planes = masks.symmetric_n(m, nx, ny, seed=7)
+    s = 2 * m + 1
+    n = nx * ny
+    B = np.zeros((n, n))
+    cc = planes[m * s + m]
+    for j in range(ny):
+        for i in range(nx):
+            k = j * nx + i
+            B[k, k] = 1.0
+            for q, c in enumerate(planes):
+                if c is None or q == m * s + m:
+                    continue
+                ii, jj = i + q % s - m, j + q // s - m
+                if 0 <= ii < nx and 0 <= jj < ny:
+                    B[k, jj * nx + ii] = c[j, i] / cc[j, i]
+    ev = np.linalg.eigvals(B)
+    assert np.max(np.abs(ev.imag)) < 1e-9
+    lo, hi = float(np.min(ev.real)), float(np.max(ev.real))
+    kmin, kmax = cjm.cjm_mask_bounds_n(planes, iters=20000)
+    assert kmax == pytest.approx(hi, rel=1e-6)
+    assert kmin == pytest.approx(lo, rel=1e-3)
+    assert kmin >= lo * (1 - 1e-9) and kmax <= hi * (1 + 1e-9)   # from inside the spectrum
