@@ -279,3 +279,23 @@ def test_maskn_sweeps_bitwise_at_bench_size(m):
     for k in range(3):
         want = oracle.maskn_sweep(planes, want, b, float(w[(7 + k) % len(w)]))
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("m", (1, 2))
+def test_maskn_variable_coefficient_solve_with_numeric_bounds(m):
+    """Symmetric variable-coefficient (2m+1)^2 mask, bounds from
+    cjm_mask_bounds_n (widened by 1%), solve to tol: converges, same
+    iterations and bitwise field as the oracle with the same bounds."""
+    nx, ny = 64, 48
+    planes = masks.symmetric_n(m, nx, ny, seed=13)
+    kmin, kmax = cjm.cjm_mask_bounds_n(planes, iters=20000)
+    kmin, kmax = 0.99 * kmin, 1.01 * kmax
+    u0, b = _field(m, nx, ny, 21)
+    u0[m:m + ny, m:m + nx] = 0.0
+    uo, ro = oracle.maskn_solve(planes, b, u0, kmin, kmax, 1e-8)
+    with cjm.MaskPlanN(nx, ny, m, kmin, kmax, 1e-8, planes=dev_planes(planes)) as plan:
+        ud = torch.from_numpy(u0.copy()).cuda()
+        rep = plan.solve(torch.from_numpy(b).cuda(), ud)
+    assert rep["status"] == "CJM_OK" and ro["status"] == "OK"
+    assert rep["iterations"] == ro["iterations"]
+    assert np.array_equal(ud.cpu().numpy(), uo)
