@@ -125,9 +125,10 @@ typedef struct {
     int band_split;        /* 1: run every K=1 hot sweep as boundary-band launches +
                               interior launch (the multi-GPU overlap schedule) even
                               without NCCL; for tests */
-    int warps;             /* variant 7 only: consumer warps per CTA, 4, 5 or 7
-                              (0 = the count that keeps the most consumer warps
-                              resident per SM) */
+    int warps;             /* variant 7 only: consumer warps per CTA, 4, 5 or 7, or 11
+                              (5/9-point at temporal_k 4: one CTA per SM); 0 = the
+                              count that keeps the most consumer warps resident per
+                              SM */
     int chunk_rows;        /* warp-tiled variants, non-reducing launches: every CTA
                               streams a static range of 80% of its share of the
                               (strip, row) units, the last 20% go out in work items of
