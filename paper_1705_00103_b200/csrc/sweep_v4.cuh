@@ -99,7 +99,7 @@ struct LaneSeg {
 // segment no ghost row (no checks); 1 = no ghost column, ghost rows possible
 // (one uniform row test per level); 0 = every node checked.
 template <int STENCIL, int NW, int K, int C, int RPS, int RI, int PH, bool REDUCE, bool STORE,
-          int FM>
+          int FM, bool STEADY = false>
 __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
                                          const SweepParams& p, const double* su, const double* sg,
                                          int st, int kk, int lane, double& acc_s, double& acc_m) {
@@ -171,7 +171,7 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
       o[j] = (FM == 2 || ((FM == 1 || ls.in[j]) && rowin)) ? __fma_rn(ws.wl[l], dd[j], uw[R])
                                                             : uw[R];
     }
-    const bool active = kk >= 2 * (l + 1) * R;
+    const bool active = STEADY || kk >= 2 * (l + 1) * R;   // STEADY: past every warm-up
     if (REDUCE && l == 0 && active && (unsigned)(G - ls.ja) < (unsigned)(ls.jb - ls.ja)) {
 #pragma unroll
       for (int j = 0; j < C; ++j)
@@ -215,7 +215,7 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
 // last stage, when GUARD), then release the stage whose rows level K-1 has
 // now read for the last time.
 template <int STENCIL, int NW, int K, int C, int RPS, int PH0, bool GUARD, bool REDUCE,
-          bool STORE, int FM>
+          bool STORE, int FM, bool STEADY = false>
 __device__ __forceinline__ void warp_stage(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
                                            const SweepParams& p, const double* su,
                                            const double* sg, int s, int kk0, int nin, int lane,
@@ -230,7 +230,8 @@ __device__ __forceinline__ void warp_stage(WarpState<Point<STENCIL>::R, K, C>& w
   if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
 #define CJM_V4_ROW(RI)                                                                         \
   if (RI < RPS && (!GUARD || kk0 + RI < nin))                                                  \
-    warp_row<STENCIL, NW, K, C, RPS, (RI < RPS ? RI : 0), (PH0 + RI) % P, REDUCE, STORE, FM>(   \
+    warp_row<STENCIL, NW, K, C, RPS, (RI < RPS ? RI : 0), (PH0 + RI) % P, REDUCE, STORE, FM,    \
+             STEADY>(                                                                          \
         ws, ls, p, su, sg, st, kk0 + RI, lane, acc_s, acc_m);
   CJM_V4_ROW(0) CJM_V4_ROW(1) CJM_V4_ROW(2) CJM_V4_ROW(3) CJM_V4_ROW(4)
 #undef CJM_V4_ROW
@@ -287,14 +288,21 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
   constexpr int U = (RPS % P == 0) ? 1 : P;
   constexpr int UR = U * RPS;
   int s0 = 0;
-  for (; (s0 + U) * RPS <= nin; s0 += U) {          // full periods: no guards
-#define CJM_V4_STAGE(u)                                                                   \
-  if (u < U)                                                                              \
-    warp_stage<STENCIL, NW, K, C, RPS, ((u < U ? u : 0) * RPS) % P, false, REDUCE, STORE, \
-               FM>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin, lane, acc_s, acc_m);
-    CJM_V4_STAGE(0) CJM_V4_STAGE(1) CJM_V4_STAGE(2) CJM_V4_STAGE(3) CJM_V4_STAGE(4)
-#undef CJM_V4_STAGE
+  // full periods, no guards: first those holding a level's warm-up rows
+  // (input rows < 2 K r), then the steady ones (every level active)
+#define CJM_V4_STAGE(u, STEADY)                                                             \
+  if (u < U)                                                                                \
+    warp_stage<STENCIL, NW, K, C, RPS, ((u < U ? u : 0) * RPS) % P, false, REDUCE, STORE, FM, \
+               STEADY>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin, lane, acc_s, acc_m);
+  for (; (s0 + U) * RPS <= nin && s0 * RPS < 2 * K * R; s0 += U) {
+    CJM_V4_STAGE(0, false) CJM_V4_STAGE(1, false) CJM_V4_STAGE(2, false) CJM_V4_STAGE(3, false)
+    CJM_V4_STAGE(4, false)
   }
+  for (; (s0 + U) * RPS <= nin; s0 += U) {
+    CJM_V4_STAGE(0, true) CJM_V4_STAGE(1, true) CJM_V4_STAGE(2, true) CJM_V4_STAGE(3, true)
+    CJM_V4_STAGE(4, true)
+  }
+#undef CJM_V4_STAGE
   static_assert(U <= 5, "stages per period <= 5");
   // tail: fewer than UR rows left, in at most U stages (rows >= nin guarded)
 #define CJM_V4_TAIL(u)                                                                     \
