@@ -102,7 +102,9 @@ template <int STENCIL, int NW, int K, int C, int RPS, int RI, int PH, bool REDUC
           int FM, bool STEADY = false>
 __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws, LaneSeg<C>& ls,
                                          const SweepParams& p, const double* su, const double* sg,
-                                         int st, int kk, int lane, double& acc_s, double& acc_m) {
+                                         int st, const double* ucur, const double* gcur,
+                                         const double* gprev, int kk, int lane, double& acc_s,
+                                         double& acc_m) {
   constexpr int R = Point<STENCIL>::R;
   constexpr int P = 2 * R + 1;
   constexpr int ph = PH;
@@ -114,7 +116,7 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
   // R(K-1) rows later (level l reads the g row that arrived with input row
   // kk - lR), so g needs no register ring.
   {
-    const double* row = su + ((size_t)st * RPS + RI) * TG_::ROW + ls.uoff;   // row[2 + j] = column j
+    const double* row = ucur + RI * TG_::ROW;   // row[2 + j] = column j
     double cc[C];
 #pragma unroll
     for (int j = 0; j < C; j += 2) {
@@ -143,9 +145,14 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
       // input row kk - lR: row GR of the stage GB stages back (compile-time)
       const int GB = (l * R - RI + RPS - 1) / RPS;  // l R <= RI: 0 (folds: l unrolled)
       const int GR = RI - l * R + GB * RPS;
-      int gs = st - GB;
-      if (gs < 0) gs += p.stages;
-      const double* grow = sg + ((size_t)gs * RPS + GR) * TG_::GROW + ls.uoff;
+      const double* grow;
+      if (RPS > 1 && GB <= 1) {            // this or the previous stage: per-stage bases
+        grow = (GB == 0 ? gcur : gprev) + GR * TG_::GROW;
+      } else {
+        int gs = st - GB;
+        if (gs < 0) gs += p.stages;
+        grow = sg + ((size_t)gs * RPS + GR) * TG_::GROW + ls.uoff;
+      }
 #pragma unroll
       for (int j = 0; j < C; j += 2) {
         const double2 v = *reinterpret_cast<const double2*>(grow + j);
@@ -228,11 +235,15 @@ __device__ __forceinline__ void warp_stage(WarpState<Point<STENCIL>::R, K, C>& w
   mbar_wait_a(ws.full_a + 8u * st, ws.phase);
 #endif
   if (++ws.stage == p.stages) { ws.stage = 0; ws.phase ^= 1u; }
+  using TG_ = TileV4<R, K, NW, C>;
+  const double* ucur = su + (size_t)st * RPS * TG_::ROW + ls.uoff;
+  const double* gcur = sg + (size_t)st * RPS * TG_::GROW + ls.uoff;
+  const double* gprev = sg + (size_t)(st == 0 ? p.stages - 1 : st - 1) * RPS * TG_::GROW + ls.uoff;
 #define CJM_V4_ROW(RI)                                                                         \
   if (RI < RPS && (!GUARD || kk0 + RI < nin))                                                  \
     warp_row<STENCIL, NW, K, C, RPS, (RI < RPS ? RI : 0), (PH0 + RI) % P, REDUCE, STORE, FM,    \
              STEADY>(                                                                          \
-        ws, ls, p, su, sg, st, kk0 + RI, lane, acc_s, acc_m);
+        ws, ls, p, su, sg, st, ucur, gcur, gprev, kk0 + RI, lane, acc_s, acc_m);
   CJM_V4_ROW(0) CJM_V4_ROW(1) CJM_V4_ROW(2) CJM_V4_ROW(3) CJM_V4_ROW(4)
 #undef CJM_V4_ROW
   static_assert(RPS <= 5, "rows per stage <= 5");
