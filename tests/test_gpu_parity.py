@@ -444,3 +444,11 @@ def test_resident_segment_bitwise(stencil, nx, ny, count):
         g = oracle.rhs_to_g(stencil, h, b)
         want = oracle.sweeps(stencil, u0, g, w, 3, count)
         assert_field_parity(host(ud), want, r)
+
+
+@pytest.mark.gpu
+def test_graft_entry_smoke():
+    """__graft_entry__.smoke(): 9-pt 64^2 and 17-pt 48^2 solves through the
+    C-ABI, bitwise equal to the oracle (the driver's round-end smoke check)."""
+    import __graft_entry__
+    __graft_entry__.smoke()
