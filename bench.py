@@ -169,7 +169,11 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     stencil, nx, nyg, tol, desc = CONFIGS[args.config]
+    import oracle
     from paper_1705_00103_b200 import inputs
+    # torchrun exports OMP_NUM_THREADS=1 to every rank; rank 0 alone works
+    # here, so it takes all host cores the process may run on
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     h = inputs.grid_h(nx, nyg)
     steps = []
     for _ in range(args.warmup + args.steps):
@@ -178,8 +182,8 @@ def run_reference(args, rank, world):
     val = statistics.median([s["value"] for s in timed])
     cb = dict(timed[-1])
     cb["value"] = val
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GLUPS", "n_gpus": 1,
-            "steps": args.steps, "warmup": args.warmup,
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GLUPS", "n_gpus": world,
+            "working_ranks": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * args.ref_seconds, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "stencil": stencil, "nx": nx, "ny": nyg,
