@@ -84,9 +84,18 @@ typedef enum {
 typedef enum { CJM_BC_DIRICHLET = 0 } cjm_bc;
 
 /* Order in which the weights of a cycle are applied (DESIGN R3; the paper is
- * silent).  LEBEDEV23 is the stable default; ASCENDING is SPEC's order
- * (S:309), unstable in fp64, offered for tests only. */
-typedef enum { CJM_ORDER_LEBEDEV23 = 0, CJM_ORDER_ASCENDING = 1 } cjm_order;
+ * silent: "precalculated ... as a transformation of the zeros").
+ * LEBEDEV23 is the stable default: cycle length P = smallest 2^a 3^b >= M_min
+ * (<= 5.2% more sweeps than M_min at every config), generalised
+ * Lebedev-Finogenov recursion.  LEBEDEV2 is the classical power-of-two case:
+ * P = smallest 2^a >= M_min (up to 2x M_min sweeps), the same recursion with
+ * factors of 2 only.  ASCENDING is SPEC's order with the 2^a 3^b
+ * cycle, unstable in fp64, offered for tests only. */
+typedef enum {
+    CJM_ORDER_LEBEDEV23 = 0,
+    CJM_ORDER_ASCENDING = 1,
+    CJM_ORDER_LEBEDEV2 = 2
+} cjm_order;
 
 /* CHEBYSHEV = the CJM.  JACOBI = the classical Jacobi baseline the
  * paper compares against (w = 1); its "cycle" is a
@@ -101,7 +110,16 @@ typedef struct {
     int world_size;        /* default 1 (single GPU) */
     int rank;              /* default 0 */
     const void *nccl_id;   /* 128-byte ncclUniqueId from cjm_get_nccl_id on rank 0,
-                              broadcast by the caller; required when world_size > 1 */
+                              broadcast by the caller; required when world_size > 1
+                              (unless external_halo).  With world_size = 1 a non-NULL
+                              id makes a ONE-rank communicator: the plan then runs the
+                              multi-GPU schedule (NCCL groups, comm-stream overlap,
+                              allreduce) on one GPU.  Communicators are cached by
+                              (id, world, rank, device): a later plan with the same id
+                              reuses the idle communicator without a collective call;
+                              every rank must make the same plan calls in the same
+                              order, and a second LIVE plan with an id in use is
+                              INVALID_ARG (ids are single-use for initialisation). */
     int device;            /* CUDA device ordinal; -1 (default) = current device */
     int external_halo;     /* world_size > 1 only: 1 = no NCCL; the caller moves the
                               halo rows itself between cjm_sweeps calls (rows from
@@ -109,11 +127,15 @@ typedef struct {
                               cjm_solve / cjm_solve_host then return UNSUPPORTED. */
     /* tuning knobs, 0 = automatic */
     int temporal_k;        /* sweeps fused per kernel launch (temporal blocking,
-                              SURVEY NEXT-1), 1..4; multi-GPU plans use 1 */
-    int variant;           /* sweep kernel, all bitwise identical: 3 = shared-line
-                              levels; warp-tiled with 4 (4) or 2 (5) columns per
-                              lane and one input row per TMA ring stage, or with
-                              2r+1 rows per stage (6: 4 columns, 7: 2 columns) */
+                              SURVEY NEXT-1), 1..4 (0 = 4 for the 5/9-point and 3 for
+                              the 17-point from 4096^2 up, one less below).  Multi-GPU
+                              plans keep K and exchange H = K r halo rows per launch
+                              (deep halos); K falls back to 1 when a slab is thinner
+                              than 2 K r + 1 rows */
+    int variant;           /* sweep kernel, both bitwise identical: 7 = warp-tiled
+                              (2 columns per lane, 2r+1 rows per TMA ring stage; the
+                              default, 17-point up to temporal_k 3); 3 = shared-line
+                              levels (the 17-point at temporal_k 4, or tile_w given) */
     int tile_w;            /* variant 3 only: tile columns per CTA, 256 or 512 */
     int ctas_per_sm;       /* resident CTAs per SM of the persistent sweep grid */
     int stages;            /* depth of the TMA ring (stages of 1 or 2r+1 rows) */
@@ -129,7 +151,7 @@ typedef struct {
                               (5/9-point at temporal_k 4: one CTA per SM); 0 = the
                               count that keeps the most consumer warps resident per
                               SM */
-    int chunk_rows;        /* warp-tiled variants, non-reducing launches: every CTA
+    int chunk_rows;        /* warp-tiled kernel, non-reducing launches: every CTA
                               streams a static range of 80% of its share of the
                               (strip, row) units, the last 20% go out in work items of
                               chunk_rows units that the CTAs take from a device counter
@@ -162,6 +184,8 @@ typedef struct {
     int variant, warps, stages, ctas;  /* launch configuration of the plan's sweep kernel:
                                           variant, consumer warps per CTA, TMA ring
                                           stages, persistent CTAs */
+    int comm_nranks;       /* ranks of the plan's NCCL communicator (0: none) */
+    int comm_rank;         /* this plan's rank in it (-1: none) */
 } cjm_report;
 
 typedef struct cjm_plan_s *cjm_plan_t;
@@ -172,8 +196,9 @@ void cjm_default_options(cjm_options *opt);
 /* Host-only scheduler (no GPU needed): SURVEY section 8(a) rows a1-a4.
  *   kappa bounds (5-pt classical S:252) at
  *   N_x = nx+1, N_y = ny+1 (DESIGN R1); M_min = ceil(acosh(1/tol)/acosh(mu))
- *   (DESIGN R5); P = smallest 2^a 3^b >= M_min and the application
- *   order t_1..t_P (DESIGN R3); w_k = 1/(kmin + (kmax-kmin) sin^2(t_k pi/4P)).
+ *   (DESIGN R5); P = smallest 2^a 3^b >= M_min (LEBEDEV2: 2^a) and
+ *   the application order t_1..t_P (DESIGN R3);
+ *   w_k = 1/(kmin + (kmax-kmin) sin^2(t_k pi/4P)).
  * Outputs: kappa_min, kappa_max, m_min, cycle_len (= P) always (nullable);
  * t_out / w_out (nullable) receive P entries if capacity >= P, else
  * CJM_ERR_INVALID_ARG (call once with capacity 0 to learn P).
@@ -332,7 +357,9 @@ cjm_status cjm_solve_host(cjm_plan_t p, const double *rhs_host, long long ld_rhs
  * uses the weight at cycle position (first + k) mod P.  u (device) is read
  * and overwritten with the result (interior only).  Used to compare a fixed
  * segment of the iteration with the oracle at any size.  rep (nullable)
- * receives sweep_s / sweeps_timed / kernel_launches. */
+ * receives sweep_s / sweeps_timed / kernel_launches.  external_halo plans
+ * (the caller moves the halos between calls): count <= temporal_k, else
+ * INVALID_ARG (a second launch would read stale neighbour rows). */
 cjm_status cjm_sweeps(cjm_plan_t p, const double *rhs, long long ld_rhs,
                       double *u, long long ld_u, long long first, long long count,
                       void *cuda_stream, cjm_report *rep);
@@ -374,13 +401,43 @@ typedef struct {
 cjm_status cjm_halo_plan(int ny, int r, int world_size, int rank, cjm_halo_msg *msgs,
                          int *nmsgs);
 
-/* Release every device buffer, graph and communicator of the plan.  NULL is
- * ok.  The field-sized buffers go to the library's device-buffer cache
- * (reused by the next plan of the same size); cjm_pool_trim frees them. */
+/* Internal buffer layout (host only): the plan's iterate / g buffers have rows
+ * of pitch *ld doubles (ld = roundup(nx + 16, 32): 256-byte aligned rows) and
+ * interior column i at *col0 + i (col0 = 8; the r ghost columns sit just left
+ * and right of the interior).  Row j of the slab (0-based, ghost rows
+ * included) starts at element j * ld.  Errors: INVALID_ARG for nx < 1. */
+cjm_status cjm_buffer_layout(int nx, long long *ld, int *col0);
+
+/* One halo transfer in elements of the internal buffer layout: send `count`
+ * doubles starting at element send_off of my buffer to `peer`, receive the
+ * peer's `count` doubles into element recv_off. */
+typedef struct {
+    int peer;
+    long long send_off;
+    long long recv_off;
+    long long count;
+} cjm_halo_xfer;
+
+/* Host-only: the transfers the library's NCCL halo exchange (row a9) issues,
+ * verbatim, for rank `rank` of `world_size` on a global grid of nx x ny
+ * interior nodes with `depth` halo rows (r, or K r for K-fused launches):
+ * cjm_halo_plan's messages as whole rows (ghost columns included) of the
+ * internal layout (cjm_buffer_layout; *ld_out nullable).  One ncclSend and
+ * one ncclRecv per transfer inside one NCCL group, on the iterate buffer the
+ * launch wrote (and once per solve on g when depth > r).  xfers must hold 2
+ * entries.  Errors as cjm_halo_plan. */
+cjm_status cjm_halo_xfers(int nx, int ny, int depth, int world_size, int rank,
+                          cjm_halo_xfer *xfers, int *nxfers, long long *ld_out);
+
+/* Release every device buffer and graph of the plan.  NULL is ok.  The
+ * field-sized buffers go to the library's device-buffer cache (reused by the
+ * next plan of the same size) and the NCCL communicator back to the
+ * communicator cache; cjm_pool_trim frees both. */
 cjm_status cjm_plan_destroy(cjm_plan_t p);
 
-/* Return every cached device buffer to the driver (cudaFree).  Call when no
- * plan is being created concurrently.  cached_bytes_before (nullable)
+/* Return every cached device buffer to the driver (cudaFree) and destroy
+ * every idle cached NCCL communicator.  Call when no plan is being created
+ * concurrently (multi-GPU: on every rank, at the same point).  cached_bytes_before (nullable)
  * receives the bytes that were cached. */
 cjm_status cjm_pool_trim(long long *cached_bytes_before);
 

@@ -69,6 +69,8 @@ def lib():
         L.oracle_m_min.restype = C.c_long
         L.oracle_cycle_len.argtypes = [C.c_long, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.oracle_cycle_len.restype = C.c_long
+        L.oracle_cycle_len_pow2.argtypes = [C.c_long, C.POINTER(C.c_int)]
+        L.oracle_cycle_len_pow2.restype = C.c_long
         L.oracle_ordering.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_long)]
         L.oracle_weights.argtypes = [C.c_double, C.c_double, C.c_long, C.POINTER(C.c_long), dp]
         L.oracle_gscale.argtypes = [C.c_int, C.c_double]
@@ -130,6 +132,12 @@ def cycle_len(m: int) -> tuple[int, int, int]:
     return int(P), a.value, b.value
 
 
+def cycle_len_pow2(m: int) -> tuple[int, int]:
+    a = C.c_int()
+    P = lib().oracle_cycle_len_pow2(m, C.byref(a))
+    return int(P), a.value
+
+
 def ordering(a: int, b: int) -> np.ndarray:
     P = 2 ** a * 3 ** b
     t = (C.c_long * P)()
@@ -144,11 +152,18 @@ def weights(kmin: float, kmax: float, t: np.ndarray) -> np.ndarray:
     return w
 
 
-def schedule(stencil: int, nx: int, ny: int, tol: float) -> dict:
-    """Steps 1-3 in one call: bounds, M, P=2^a3^b, ordering t, weights w."""
+def schedule(stencil: int, nx: int, ny: int, tol: float, order: str = "lebedev23") -> dict:
+    """Steps 1-3 in one call: bounds, M, P=2^a3^b (order "lebedev2": P=2^a),
+    ordering t, weights w."""
     kmin, kmax = bounds(stencil, nx, ny)
     m = m_min(kmin, kmax, tol)
-    P, a, b = cycle_len(m)
+    if order == "lebedev2":
+        P, a = cycle_len_pow2(m)
+        b = 0
+    elif order == "lebedev23":
+        P, a, b = cycle_len(m)
+    else:
+        raise ValueError(order)
     t = ordering(a, b)
     return dict(kappa_min=kmin, kappa_max=kmax, m_min=m, P=P, a=a, b=b, t=t,
                 w=weights(kmin, kmax, t))

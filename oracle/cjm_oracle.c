@@ -143,6 +143,17 @@ long oracle_cycle_len(long m_min, int *a_out, int *b_out)
     return best;
 }
 
+/* Step 2b': the power-of-two cycle of the classical Lebedev-Finogenov
+ * ordering (order option LEBEDEV2, DESIGN R3): P = the smallest 2^a >= M. */
+long oracle_cycle_len_pow2(long m_min, int *a_out)
+{
+    long p = 1;
+    int a = 0;
+    while (p < m_min) { p *= 2; a++; }
+    *a_out = a;
+    return p;
+}
+
 /* Step 3a: order in which the P Chebyshev zeros are applied (DESIGN R3).
  * The paper does not state an order; this is the Lebedev-Finogenov
  * recursion generalised to P = 2^a 3^b.  Start from the list [1] with m = 1;

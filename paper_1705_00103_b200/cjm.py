@@ -25,7 +25,7 @@ LIB_PATH = os.environ.get("CJM_LIB") or os.path.join(HERE, "libcjm.so")
 
 STENCIL_MASK, STENCIL_5, STENCIL_9, STENCIL_17 = 1, 5, 9, 17
 BC_DIRICHLET = 0
-ORDER_LEBEDEV23, ORDER_ASCENDING = 0, 1
+ORDER_LEBEDEV23, ORDER_ASCENDING, ORDER_LEBEDEV2 = 0, 1, 2
 METHOD_CHEBYSHEV, METHOD_JACOBI = 0, 1
 
 STATUS = {0: "CJM_OK", 1: "CJM_ERR_INVALID_ARG", 2: "CJM_ERR_UNSUPPORTED",
@@ -38,7 +38,7 @@ EXPORTS = ("cjm_default_options", "cjm_schedule", "cjm_plan", "cjm_plan_info", "
            "cjm_solve_host", "cjm_sweeps", "cjm_residual", "cjm_get_nccl_id", "cjm_slab", "cjm_halo_plan",
            "cjm_plan_destroy", "cjm_pool_trim", "cjm_status_str", "cjm_last_error", "cjm_version",
            "cjm_plan_mask", "cjm_mask_set", "cjm_mask_bounds", "cjm_plan_mask_n", "cjm_mask_set_n",
-           "cjm_mask_bounds_n")
+           "cjm_mask_bounds_n", "cjm_buffer_layout", "cjm_halo_xfers")
 
 
 class CJMError(RuntimeError):
@@ -63,6 +63,11 @@ class HaloMsg(C.Structure):
     _fields_ = [("peer", C.c_int), ("send_row", C.c_int), ("recv_row", C.c_int), ("rows", C.c_int)]
 
 
+class HaloXfer(C.Structure):
+    _fields_ = [("peer", C.c_int), ("send_off", C.c_longlong), ("recv_off", C.c_longlong),
+                ("count", C.c_longlong)]
+
+
 class Report(C.Structure):
     _fields_ = [("iterations", C.c_longlong), ("cycles", C.c_int), ("status", C.c_int),
                 ("cycle_len", C.c_longlong), ("m_min", C.c_longlong),
@@ -74,7 +79,8 @@ class Report(C.Structure):
                 ("hot_launches", C.c_longlong), ("temporal_k", C.c_int), ("resident", C.c_int),
                 ("ghost_rows", C.c_int), ("rhs_ghost_rows", C.c_int),
                 ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("real_error", C.c_double),
-                ("variant", C.c_int), ("warps", C.c_int), ("stages", C.c_int), ("ctas", C.c_int)]
+                ("variant", C.c_int), ("warps", C.c_int), ("stages", C.c_int), ("ctas", C.c_int),
+                ("comm_nranks", C.c_int), ("comm_rank", C.c_int)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -117,6 +123,8 @@ def lib():
     L.cjm_get_nccl_id.argtypes = [vp]
     L.cjm_slab.argtypes = [i, i, i, C.POINTER(i), C.POINTER(i)]
     L.cjm_halo_plan.argtypes = [i, i, i, i, C.POINTER(HaloMsg), C.POINTER(i)]
+    L.cjm_buffer_layout.argtypes = [i, C.POINTER(ll), C.POINTER(i)]
+    L.cjm_halo_xfers.argtypes = [i, i, i, i, i, C.POINTER(HaloXfer), C.POINTER(i), C.POINTER(ll)]
     L.cjm_plan_destroy.argtypes = [vp]
     L.cjm_pool_trim.argtypes = [C.POINTER(ll)]
     L.cjm_status_str.argtypes = [i]
@@ -202,6 +210,24 @@ def cjm_halo_plan(ny: int, r: int, world_size: int, rank: int) -> list[dict]:
     _check(lib().cjm_halo_plan(ny, r, world_size, rank, msgs, C.byref(n)), "cjm_halo_plan")
     return [dict(peer=m.peer, send_row=m.send_row, recv_row=m.recv_row, rows=m.rows)
             for m in msgs[:n.value]]
+
+
+def cjm_buffer_layout(nx: int) -> tuple[int, int]:
+    """(ld, col0) of the library's internal row layout for nx interior columns."""
+    ld, c0 = C.c_longlong(), C.c_int()
+    _check(lib().cjm_buffer_layout(nx, C.byref(ld), C.byref(c0)), "cjm_buffer_layout")
+    return ld.value, c0.value
+
+
+def cjm_halo_xfers(nx: int, ny: int, depth: int, world_size: int, rank: int) -> tuple[list[dict], int]:
+    """The element-level transfers of the library's NCCL halo exchange
+    (peer, send_off, recv_off, count in doubles of the internal layout) and ld."""
+    xs = (HaloXfer * 2)()
+    n, ld = C.c_int(), C.c_longlong()
+    _check(lib().cjm_halo_xfers(nx, ny, depth, world_size, rank, xs, C.byref(n), C.byref(ld)),
+           "cjm_halo_xfers")
+    return [dict(peer=x.peer, send_off=x.send_off, recv_off=x.recv_off, count=x.count)
+            for x in xs[:n.value]], ld.value
 
 
 def cjm_get_nccl_id() -> bytes:
@@ -424,7 +450,15 @@ def cjm_mask_bounds_n(planes: list, iters: int = 0) -> tuple[float, float]:
     if m is None:
         raise ValueError("a square mask has 9 or 25 planes")
     arrs = [None if c is None else np.ascontiguousarray(c, dtype=np.float64) for c in planes]
-    ny, nx = arrs[m * (2 * m + 1) + m].shape
+    centre = arrs[m * (2 * m + 1) + m]
+    if centre is None:
+        raise ValueError("the centre plane c_C is required")
+    if centre.ndim != 2:
+        raise ValueError("planes must be 2-D (ny, nx) arrays")
+    ny, nx = centre.shape
+    for k, a in enumerate(arrs):
+        if a is not None and a.shape != (ny, nx):
+            raise ValueError(f"planes[{k}]: shape {a.shape}, centre plane is {(ny, nx)}")
     ptrs = (C.c_void_p * q)(*[None if a is None else a.ctypes.data for a in arrs])
     kmin, kmax = C.c_double(), C.c_double()
     _check(lib().cjm_mask_bounds_n(nx, ny, m, ptrs, nx, iters, C.byref(kmin), C.byref(kmax)),

@@ -125,14 +125,15 @@ using cjm::MODE_CHECK;
 using cjm::MODE_RESID;
 using cjm::KernelFn;
 
-// nw: consumer warps per CTA (variant 7 only: 4, 5 or 7).  The instantiations
-// live in kernels_*.cu (compiled in parallel).
+// variant 7: the warp-tiled kernel, nw consumer warps per CTA (4, 5, 7 or
+// 11); variant 3: the shared-line kernel, NT threads.  The instantiations
+// live in kernels_*.cu (compiled in parallel); nullptr = not instantiated.
 KernelFn pick_kernel(int stencil, int variant, int NT, int K, int mode, int nw = 4) {
-  if (variant >= 4) {
+  if (variant == 7) {
     switch (stencil) {
-      case 5: return cjm::pick_sweep_v4_5(variant, K, mode, nw);
-      case 9: return cjm::pick_sweep_v4_9(variant, K, mode, nw);
-      default: return cjm::pick_sweep_v4_17(variant, K, mode, nw);
+      case 5: return cjm::pick_sweep_v4_5(K, mode, nw);
+      case 9: return cjm::pick_sweep_v4_9(K, mode, nw);
+      default: return cjm::pick_sweep_v4_17(K, mode, nw);
     }
   }
   return cjm::pick_sweep_v3(stencil, NT, K, mode);
@@ -182,7 +183,6 @@ struct cjm_plan_s {
   // distribution
   int world = 1, rank = 0, device = 0;
   ncclComm_t comm = nullptr;
-  bool owns_comm = false;   // comm not in the cache: destroyed with the plan
   // device memory
   long long ld = 0;
   size_t buf_elems = 0, g_elems = 0;
@@ -206,7 +206,7 @@ struct cjm_plan_s {
   size_t small_bytes = 0;
   // launch configuration
   int NT = 128, K = 1, stages = 8, nctas = 0, ctas_per_sm = 2, graph_chunk = 64;
-  int variant = 4;   // 3: shared-line levels (sweep.cuh), 4-7: warp-tiled (sweep_v4.cuh)
+  int variant = 7;   // 3: shared-line levels (sweep.cuh), 7: warp-tiled (sweep_v4.cuh)
   int nw = 4;        // consumer warps per CTA (warp-tiled)
   int chunk_rows = -1;  // warp-tiled hot launches: rows per dynamically scheduled work item
                         // (0: static ranges, -1: chosen per launch)
@@ -232,8 +232,9 @@ struct cjm_plan_s {
 
 namespace {
 
-int v4_cpl(int variant) { return (variant == 5 || variant == 7) ? 2 : 4; }
-int v4_rps(int variant, int R) { return variant >= 6 ? 2 * R + 1 : 1; }   // rows per ring stage
+// warp-tiled kernel: 2 columns per lane, 2r+1 input rows per TMA ring stage
+constexpr int V4_CPL = 2;
+int v4_rps(int R) { return 2 * R + 1; }
 
 int v4_tout(int R, int K, int C, int nw) {   // owned columns per CTA strip, warp-tiled variant
   const int E = K == 1 ? 0 : ((R * (K - 1) + 1) & ~1);
@@ -241,18 +242,18 @@ int v4_tout(int R, int K, int C, int nw) {   // owned columns per CTA strip, war
 }
 
 int tile_out(const cjm_plan_s* pl, int K) {
-  if (pl->variant >= 4) return v4_tout(pl->R, K, v4_cpl(pl->variant), pl->nw);
+  if (pl->variant == 7) return v4_tout(pl->R, K, V4_CPL, pl->nw);
   return 2 * pl->NT - 2 * tile_e(pl->R, K);
 }
 
 size_t smem_bytes(const cjm_plan_s* pl, int K) {
-  if (pl->variant >= 4) {
-    const int C = v4_cpl(pl->variant);
+  if (pl->variant == 7) {
+    const int C = V4_CPL;
     const int E = K == 1 ? 0 : ((pl->R * (K - 1) + 1) & ~1);
     const int WOUT = 32 * C - 2 * E;
     const int TG = (pl->nw - 1) * WOUT + 32 * C;
     const int ROW = (TG + 4 + 7) / 8 * 8, GROW = (TG + 7) / 8 * 8;
-    return (size_t)pl->stages * v4_rps(pl->variant, pl->R) * (ROW + GROW) * sizeof(double) +
+    return (size_t)pl->stages * v4_rps(pl->R) * (ROW + GROW) * sizeof(double) +
            2 * (size_t)pl->stages * sizeof(uint64_t);
   }
   const int T = 2 * pl->NT, ROW = T + 8;
@@ -261,7 +262,7 @@ size_t smem_bytes(const cjm_plan_s* pl, int K) {
          2 * (size_t)pl->stages * sizeof(uint64_t);
 }
 
-int block_threads(const cjm_plan_s* pl) { return pl->variant >= 4 ? pl->nw * 32 + 32 : pl->NT + 32; }
+int block_threads(const cjm_plan_s* pl) { return pl->variant == 7 ? pl->nw * 32 + 32 : pl->NT + 32; }
 
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur.
 // One sweep-kernel launch of K fused sweeps reading buffer host_cur, over the
@@ -349,7 +350,7 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int ro
   int chunk = 0;
   long long ustat = sp.units;
   const long long per_cta = sp.units / std::max(grid, 1);
-  if (mode == MODE_HOT && pl->variant >= 4 &&
+  if (mode == MODE_HOT && pl->variant == 7 &&
       (pl->chunk_rows > 0 || (pl->chunk_rows < 0 && per_cta >= 64))) {
     // (auto: small grids, e.g. 1024^2 with 14 rows per CTA, stay static --
     // 21.3 vs 27.7 ms per 9-point solve)
@@ -372,17 +373,17 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int ro
 // (r rows x ld doubles, ghost columns included: they hold the same Dirichlet
 // data on both ranks).
 cjm_status halo_exchange(cjm_plan_s* pl, double* b, cudaStream_t st) {
-  if (pl->world == 1 || !pl->comm) return CJM_OK;   // external_halo: the caller moves them
-  cjm_halo_msg msgs[2];
-  int nm = 0;
-  STATUS_TRY(cjm_halo_plan(pl->ny, pl->H, pl->world, pl->rank, msgs, &nm));
+  if (!pl->comm) return CJM_OK;   // single GPU, or external_halo: the caller moves them
+  // the element-level transfer list of cjm_halo_xfers, executed verbatim (a
+  // one-rank communicator has none: an empty NCCL group)
+  cjm_halo_xfer xs[2];
+  int nx_ = 0;
+  long long ld = 0;
+  if (pl->world > 1) STATUS_TRY(cjm_halo_xfers(pl->nx, pl->ny, pl->H, pl->world, pl->rank, xs, &nx_, &ld));
   NCCL_TRY(ncclGroupStart());
-  for (int k = 0; k < nm; ++k) {
-    const size_t cnt = (size_t)msgs[k].rows * pl->ld;
-    NCCL_TRY(ncclSend(b + (long long)msgs[k].send_row * pl->ld, cnt, ncclDouble, msgs[k].peer,
-                      pl->comm, st));
-    NCCL_TRY(ncclRecv(b + (long long)msgs[k].recv_row * pl->ld, cnt, ncclDouble, msgs[k].peer,
-                      pl->comm, st));
+  for (int k = 0; k < nx_; ++k) {
+    NCCL_TRY(ncclSend(b + xs[k].send_off, (size_t)xs[k].count, ncclDouble, xs[k].peer, pl->comm, st));
+    NCCL_TRY(ncclRecv(b + xs[k].recv_off, (size_t)xs[k].count, ncclDouble, xs[k].peer, pl->comm, st));
   }
   NCCL_TRY(ncclGroupEnd());
   return CJM_OK;
@@ -421,7 +422,7 @@ cjm_status sweep_and_exchange(cjm_plan_s* pl, int mode, int K, cudaStream_t st) 
 // Multi-GPU: the NCCL buffers depend on the starting buffer parity.
 cjm_status get_graph(cjm_plan_s* pl, long long len, int K, cudaGraphExec_t* out,
                      long long* kernels) {
-  const int par = pl->world > 1 ? pl->host_cur : 0;
+  const int par = pl->comm ? pl->host_cur : 0;
   const std::pair<long long, int> key{len * 8 + K, par};
   auto it = pl->graphs.find(key);
   if (it != pl->graphs.end()) {
@@ -524,7 +525,7 @@ cjm_status run_hot(cjm_plan_s* pl, long long count, cudaStream_t st, long long* 
 
 // Sum / max over ranks of the reduction result and D2H of the two scalars.
 cjm_status fetch_result(cjm_plan_s* pl, cudaStream_t st, double* s, double* m) {
-  if (pl->world > 1 && pl->comm) {
+  if (pl->comm) {
     NCCL_TRY(ncclGroupStart());
     NCCL_TRY(ncclAllReduce(pl->result, pl->result, 1, ncclDouble, ncclSum, pl->comm, st));
     NCCL_TRY(ncclAllReduce(pl->result + 1, pl->result + 1, 1, ncclDouble, ncclMax, pl->comm, st));
@@ -547,7 +548,7 @@ cjm_status real_error(cjm_plan_s* pl, int which, const double* ref, long long ld
                                                 pl->ny_local, pl->err_bits);
   CUDA_TRY(cudaGetLastError());
   pl->launches += 1;
-  if (pl->world > 1 && pl->comm) {
+  if (pl->comm) {
     double* d = reinterpret_cast<double*>(pl->err_bits);
     NCCL_TRY(ncclAllReduce(d, d, 1, ncclDouble, ncclMax, pl->comm, st));
   }
@@ -631,11 +632,18 @@ void fill_static(const cjm_plan_s* pl, cjm_report* r) {
   r->temporal_k = pl->K;
   r->resident = pl->resident;
   r->variant = pl->variant;
-  r->warps = pl->variant >= 4 ? pl->nw : pl->NT / 32;
+  r->warps = pl->variant == 7 ? pl->nw : pl->NT / 32;
   r->stages = pl->stages;
   r->ctas = pl->nctas;
   r->ghost_rows = pl->Hu;
   r->rhs_ghost_rows = pl->Hr;
+  if (pl->comm) {
+    ncclCommCount(pl->comm, &r->comm_nranks);
+    ncclCommUserRank(pl->comm, &r->comm_rank);
+  } else {
+    r->comm_nranks = 0;
+    r->comm_rank = -1;
+  }
 }
 
 // The whole solve (rows a5-a10); `kin` / `kout` select device or host user buffers.
@@ -658,8 +666,9 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
   fill_static(pl, &rep);
   const double sc = std::fabs(pl->gscale);
   pl->launches = 0;
-  // the check launch fuses Kc sweeps; the hot part of a cycle is P - Kc sweeps
-  const int Kc = (int)std::min<long long>(pl->K, pl->P);
+  // the check launch fuses Kc sweeps (K, or 1 when a cycle is shorter than K:
+  // only K and 1 are configured launches); the hot part of a cycle is P - Kc
+  const int Kc = pl->P >= pl->K ? pl->K : 1;
 
   CUDA_TRY(cudaEventRecord(pl->ev[0], st));
   STATUS_TRY(stage_in(pl, rhs, ld_rhs, u, ld_u, true, kin, st));
@@ -758,7 +767,7 @@ cjm_status cjm_schedule(int stencil, int nx, int ny, double tol, int order, doub
                         double* kappa_max, long long* m_min, long long* cycle_len,
                         long long* t_out, double* w_out, long long capacity) {
   if (!cjm::stencil_reach(stencil) || nx < 4 || ny < 4 || !(tol > 0.0 && tol < 1.0) ||
-      (order != CJM_ORDER_LEBEDEV23 && order != CJM_ORDER_ASCENDING)) {
+      (order != CJM_ORDER_LEBEDEV23 && order != CJM_ORDER_ASCENDING && order != CJM_ORDER_LEBEDEV2)) {
     set_error("cjm_schedule", "invalid argument");
     return CJM_ERR_INVALID_ARG;
   }
@@ -817,6 +826,34 @@ cjm_status cjm_halo_plan(int ny, int r, int world_size, int rank, cjm_halo_msg* 
   return CJM_OK;
 }
 
+cjm_status cjm_buffer_layout(int nx, long long* ld, int* col0) {
+  if (nx < 1) return CJM_ERR_INVALID_ARG;
+  if (ld) *ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
+  if (col0) *col0 = cjm::PADL;
+  return CJM_OK;
+}
+
+cjm_status cjm_halo_xfers(int nx, int ny, int depth, int world_size, int rank, cjm_halo_xfer* xfers,
+                          int* nxfers, long long* ld_out) {
+  cjm_halo_msg msgs[2];
+  int nm = 0;
+  long long ld = 0;
+  if (!xfers || !nxfers || cjm_buffer_layout(nx, &ld, nullptr) != CJM_OK) {
+    set_error("cjm_halo_xfers", "invalid argument");
+    return CJM_ERR_INVALID_ARG;
+  }
+  STATUS_TRY(cjm_halo_plan(ny, depth, world_size, rank, msgs, &nm));
+  for (int k = 0; k < nm; ++k) {
+    xfers[k].peer = msgs[k].peer;
+    xfers[k].send_off = (long long)msgs[k].send_row * ld;
+    xfers[k].recv_off = (long long)msgs[k].recv_row * ld;
+    xfers[k].count = (long long)msgs[k].rows * ld;   // whole rows, ghost columns included
+  }
+  *nxfers = nm;
+  if (ld_out) *ld_out = ld;
+  return CJM_OK;
+}
+
 cjm_status cjm_get_nccl_id(void* out128) {
   if (!out128) return CJM_ERR_INVALID_ARG;
   ncclUniqueId id;
@@ -850,9 +887,7 @@ cjm_status cjm_plan_destroy(cjm_plan_t p) {
   if (p->res_halo) cjm::pool_free(p->device, p->res_halo_bytes, p->res_halo);
   if (p->res_flags) cjm::pool_free(p->device, (size_t)p->res_ctas * sizeof(unsigned int), p->res_flags);
   cjm::pool_free_host(2 * sizeof(double), p->result_host);
-  if (p->comm && p->owns_comm) {
-    ncclCommDestroy(p->comm);
-  } else if (p->comm) {   // back to the communicator cache (destroyed by cjm_pool_trim)
+  if (p->comm) {   // back to the communicator cache (destroyed by cjm_pool_trim)
     std::lock_guard<std::mutex> lk(g_comm_mu);
     for (auto& kv : g_comms)
       if (kv.second.first == p->comm) kv.second.second -= 1;
@@ -877,6 +912,12 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     return CJM_ERR_UNSUPPORTED;
   }
   const bool mask = stencil == CJM_STENCIL_MASK;
+  // NCCL data plane: world_size > 1 without external_halo, or a one-rank
+  // communicator requested by passing an id with world_size = 1 (runs the
+  // multi-GPU schedule -- comm stream, band split, NCCL groups, allreduce --
+  // on one GPU)
+  const bool use_nccl = !mask && ((opt.world_size > 1 && !opt.external_halo) ||
+                                  (opt.world_size == 1 && opt.nccl_id));
   if (mask && opt.world_size != 1) {
     set_error("cjm_plan_mask", "generic-mask plans are single-GPU");
     return CJM_ERR_UNSUPPORTED;
@@ -888,7 +929,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
       (opt.method != CJM_METHOD_CHEBYSHEV && opt.method != CJM_METHOD_JACOBI) ||
       (opt.tile_w != 0 && opt.tile_w != 256 && opt.tile_w != 512) || opt.stages < 0 ||
       opt.temporal_k < 0 || opt.temporal_k > 4 ||
-      (opt.variant != 0 && (opt.variant < 3 || opt.variant > 7)) ||
+      (opt.variant != 0 && opt.variant != 3 && opt.variant != 7) ||
       opt.stages > 32 || opt.ctas_per_sm < 0 || opt.graph_chunk < 0 || opt.max_cycles < 0 ||
       opt.jacobi_check < 0) {
     set_error("cjm_plan", "invalid argument");
@@ -995,19 +1036,17 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   // multi-GPU: K-fused launches need H = K r deep halos, exchanged after every
   // launch; the slab must stay thicker than 2H + 1 rows (else fall back to K=1)
   if (pl->world > 1 && nyl < 2 * pl->K * R + 1) pl->K = 1;
-  if (stencil == 17 && pl->K > 1 && pl->variant >= 4) {
-    if (v4_cpl(pl->variant) == 4 || pl->K > (pl->variant == 7 ? 3 : 2)) {
-      if (opt.variant >= 4) {
-        set_error("cjm_plan", "warp-tiled variants run the 17-point with temporal_k <= 2 (variant 5) "
-                              "or <= 3 (variant 7) only");
-        return fail(CJM_ERR_INVALID_ARG);
-      }
-      pl->variant = 3;
+  if (stencil == 17 && pl->K > 3 && pl->variant == 7) {
+    // the warp-tiled kernel runs the 17-point with temporal_k <= 3 (register
+    // rings); temporal_k = 4 is the shared-line kernel's
+    if (opt.variant == 7) {
+      set_error("cjm_plan", "variant 7 runs the 17-point with temporal_k <= 3 only");
+      return fail(CJM_ERR_INVALID_ARG);
     }
+    pl->variant = 3;
   }
   pl->stages = opt.stages > 0 ? opt.stages
-                              : (pl->variant >= 6 ? (R == 1 ? 6 : 4)
-                                                  : pl->variant >= 4 ? 8 : (pl->NT == 256 ? 12 : 4));
+                              : (pl->variant == 7 ? (R == 1 ? 6 : 4) : (pl->NT == 256 ? 12 : 4));
   pl->graph_chunk = opt.graph_chunk > 0 ? opt.graph_chunk : 64;
   pl->chunk_rows = opt.chunk_rows > 0 ? opt.chunk_rows : (opt.chunk_rows < 0 ? 0 : -1);   // -1: auto
   if (const char* e = std::getenv("CJM_DYN_PCT")) pl->dyn_pct = std::max(0, std::min(100, std::atoi(e)));
@@ -1057,12 +1096,11 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     pl->nw = best_nw;
     pl->stages = best_st;
   }
-  if (pl->variant >= 4 &&
-      pl->stages < ((pl->K - 1) * R + v4_rps(pl->variant, R) - 1) / v4_rps(pl->variant, R) + 2) {
+  if (pl->variant == 7 && pl->stages < ((pl->K - 1) * R + v4_rps(R) - 1) / v4_rps(R) + 2) {
     // the warp-tiled kernel holds a stage until level K-1 has read the g rows
     // of its rows, R(K-1) rows later
     set_error("cjm_plan", "stages must be >= ceil(r(temporal_k-1) / rows_per_stage) + 2 for the "
-                          "warp-tiled variants");
+                          "warp-tiled kernel");
     return fail(CJM_ERR_INVALID_ARG);
   }
   if (smem_bytes(pl, pl->K) > (size_t)smem_optin - 2048) {
@@ -1075,6 +1113,10 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     for (int mode = 0; mode < 3; ++mode) {
       if (mode == MODE_RESID && K != 1) continue;
       KernelFn k = pick_kernel(stencil, pl->variant, pl->NT, K, mode, pl->nw);
+      if (!k) {   // every launch the executor can issue must be instantiated
+        set_error("cjm_plan", "no sweep kernel instantiated for this (stencil, temporal_k, warps)");
+        return fail(CJM_ERR_INVALID_ARG);
+      }
       const size_t sm = smem_bytes(pl, K);
       PLAN_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sm));
@@ -1092,13 +1134,13 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   // exchange, which overlaps the interior band launch (a persistent grid on
   // every SM would leave them no slot: the warp-tiled kernels fill the
   // register file); the dynamic work items absorb the lost SMs
-  const int reserve = (pl->world > 1 && !opt.external_halo && nsm > 8) ? 2 : 0;
+  const int reserve = (use_nccl && nsm > 8) ? 2 : 0;
   pl->nctas = (nsm - reserve) * std::min(occ_min, pl->ctas_per_sm);
   }
 
   // ---- resident (shared-memory) hot path: single GPU, whole grid fits in the
   // SMs' shared memory with at least 16 rows per CTA
-  if (pl->world == 1 && opt.resident >= 0 && !mask) {
+  if (pl->world == 1 && !use_nccl && opt.resident >= 0 && !mask) {
     const int ldS = nx + 2 * R;
     auto smem_for = [&](int rows) {
       return ((size_t)2 * (rows + 2 * R) * ldS + (size_t)rows * nx) * sizeof(double);
@@ -1106,8 +1148,12 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     // at least 16 rows per CTA for small grids (fewer handshakes), else the
     // minimum slab height that spreads the grid over all SMs
     const int rows_min = (nyl + nsm - 1) / nsm;
+    // (every CTA but the last must own >= R rows: a CTA publishes its first /
+    // last R rows to its neighbours, and a thinner slab would publish one of
+    // its own ghost rows, a stale copy of the neighbour's data)
     int rows = std::max(rows_min, std::min(16, nyl));
     if (smem_for(rows) + 1024 > (size_t)smem_optin) rows = rows_min;
+    rows = std::max(rows, std::min(R, nyl));
     // the whole grid in ONE CTA when it fits: no handshakes at all
     if (smem_for(nyl) + 1024 <= (size_t)smem_optin) rows = nyl;
     const int ctas = (nyl + rows - 1) / rows;
@@ -1137,7 +1183,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
 
   tt.mark("schedule+config");
   // ---- buffers: (ny_local + 2R) rows of pitch ld; interior column 0 at PADL
-  pl->ld = ((long long)nx + 2 * cjm::PADL + 31) / 32 * 32;
+  cjm_buffer_layout(nx, &pl->ld, nullptr);
   pl->H = pl->world > 1 ? pl->K * R : R;
   const bool deep_external = pl->world > 1 && opt.external_halo && pl->K > 1;
   pl->Hu = deep_external ? pl->H : R;
@@ -1184,7 +1230,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   PLAN_CUDA(cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming));
   for (auto& e : pl->ev) PLAN_CUDA(cudaEventCreate(&e));
 
-  if (pl->world > 1 && !opt.external_halo) {
+  if (use_nccl) {
     ncclUniqueId id;
     std::memcpy(&id, opt.nccl_id, sizeof(id));
     CommKey key;
@@ -1192,26 +1238,41 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
     key.world = pl->world;
     key.rank = pl->rank;
     key.device = dev;
+    // Cache decision: a cached, idle communicator for this id is reused (no
+    // collective call); an unknown id is initialised (ncclCommInitRank, a
+    // collective over the world).  Every rank makes the same plan calls in
+    // the same order, so the decisions agree across ranks.  An id is
+    // single-use for initialisation: a second LIVE plan with the same id
+    // cannot get a communicator (re-initialising a consumed id would hang)
+    // and is rejected -- pass a fresh cjm_get_nccl_id() for concurrent plans.
+    bool init = false;
     {
       std::lock_guard<std::mutex> lk(g_comm_mu);
       auto it = g_comms.find(key);
-      if (it != g_comms.end() && it->second.second == 0) {
+      if (it == g_comms.end()) {
+        init = true;
+        g_comms[key] = {nullptr, 1};   // reserved while this plan initialises it
+      } else if (it->second.second == 0 && it->second.first) {
         pl->comm = it->second.first;
         it->second.second = 1;
       }
     }
-    if (!pl->comm) {
-      ncclResult_t r = ncclCommInitRank(&pl->comm, pl->world, id, pl->rank);
+    if (!pl->comm && !init) {
+      set_error("cjm_plan", "a live plan already uses this NCCL id (ids are single-use: pass a fresh "
+                            "cjm_get_nccl_id for concurrent plans)");
+      return fail(CJM_ERR_INVALID_ARG);
+    }
+    if (init) {
+      ncclComm_t c = nullptr;
+      ncclResult_t r = ncclCommInitRank(&c, pl->world, id, pl->rank);
+      std::lock_guard<std::mutex> lk(g_comm_mu);
       if (r != ncclSuccess) {
+        g_comms.erase(key);
         set_error("ncclCommInitRank", ncclGetErrorString(r));
-        pl->comm = nullptr;
         return fail(CJM_ERR_NCCL);
       }
-      std::lock_guard<std::mutex> lk(g_comm_mu);
-      auto it = g_comms.find(key);
-      if (it == g_comms.end()) g_comms[key] = {pl->comm, 1};
-      // (a second live plan with the same id keeps its own, uncached comm)
-      else pl->owns_comm = true;
+      g_comms[key] = {c, 1};
+      pl->comm = c;
     }
   }
 
@@ -1371,6 +1432,12 @@ cjm_status cjm_sweeps(cjm_plan_t p, const double* rhs, long long ld_rhs, double*
                       long long first, long long count, void* cuda_stream, cjm_report* rep_out) {
   if (!check_layout(p, rhs, ld_rhs, u, ld_u) || !rhs || first < 0 || count < 0) {
     set_error("cjm_sweeps", "invalid argument");
+    return CJM_ERR_INVALID_ARG;
+  }
+  if (p->world > 1 && !p->comm && count > p->K) {
+    // external_halo: the caller refreshes the halos between calls; more than
+    // one launch per call would read stale neighbour rows
+    set_error("cjm_sweeps", "external_halo plans apply at most temporal_k sweeps per call");
     return CJM_ERR_INVALID_ARG;
   }
   CUDA_TRY(cudaSetDevice(p->device));

@@ -14,9 +14,10 @@ using KernelFn = void (*)(const SweepParams);
 
 // shared-line kernel (variant 3, sweep.cuh), NT = 128 or 256 threads
 KernelFn pick_sweep_v3(int stencil, int NT, int K, int mode);
-// warp-tiled kernels (variants 4-7, sweep_v4.cuh), one file per stencil
-KernelFn pick_sweep_v4_5(int variant, int K, int mode, int nw);
-KernelFn pick_sweep_v4_9(int variant, int K, int mode, int nw);
-KernelFn pick_sweep_v4_17(int variant, int K, int mode, int nw);
+// warp-tiled kernel (variant 7, sweep_v4.cuh), one file per stencil; nw =
+// consumer warps per CTA
+KernelFn pick_sweep_v4_5(int K, int mode, int nw);
+KernelFn pick_sweep_v4_9(int K, int mode, int nw);
+KernelFn pick_sweep_v4_17(int K, int mode, int nw);
 
 }  // namespace cjm

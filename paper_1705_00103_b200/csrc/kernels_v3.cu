@@ -31,16 +31,11 @@ KernelFn pick_nt(int NT, int K, int mode) {
 }  // namespace
 
 KernelFn pick_sweep_v3(int stencil, int NT, int K, int mode) {
-#ifdef CJM_EXPERIMENT_9PT_V7
-  (void)stencil; (void)NT; (void)K; (void)mode;
-  return nullptr;
-#else
   switch (stencil) {
     case 5: return pick_nt<5>(NT, K, mode);
     case 9: return pick_nt<9>(NT, K, mode);
     default: return pick_nt<17>(NT, K, mode);
   }
-#endif
 }
 
 }  // namespace cjm

@@ -5,6 +5,7 @@
 // cycle length  : M_min = ceil(acosh(1/tol) / acosh(mu)), mu = (kmax+kmin)/
 //                 (kmax-kmin) ("depends on ... the required tolerance";
 //                 S:292), acosh(mu) via log1p (DESIGN R5); P = min 2^a 3^b >= M
+//                 (CJM_ORDER_LEBEDEV2: P = min 2^a >= M)
 // ordering      : generalised Lebedev-Finogenov recursion (DESIGN R3)
 // weights       : w = 1/(kmin + (kmax-kmin) sin^2(t pi / 4P))  (the
 //                 half-angle form of S:292's 2/[(kmax+kmin)-(kmax-kmin)cos])
@@ -109,7 +110,12 @@ bool build_schedule_bounds(double kmin, double kmax, double tol, int order, Sche
   s->m_min = chebyshev_degree(s->kmin, s->kmax, tol);
   int a = 0, b = 0;
   s->P = smooth_cycle_length(s->m_min, &a, &b);
-  if (order == 0) {
+  if (order == 2) {   // power-of-two cycle: P = smallest 2^a >= M_min
+    a = 0;
+    b = 0;
+    for (s->P = 1; s->P < s->m_min; s->P *= 2) ++a;
+  }
+  if (order == 0 || order == 2) {
     s->t = lebedev23_order(a, b);
   } else if (order == 1) {  // ascending weights = descending zero index
     s->t.resize(s->P);

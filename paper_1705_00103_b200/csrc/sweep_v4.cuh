@@ -348,14 +348,8 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
 // 17-point) keep one CTA per SM and are not capped.
 template <int STENCIL, int K, int C>
 struct V4Regs {
-#ifdef CJM_X_NW7_NOCAP   // experiment: 7 consumer warps (one CTA per SM) without the cap
-  static constexpr int value = 255;
-#elif defined(CJM_X_CAP128)   // experiment: 4 warps per sub-partition
-  static constexpr int value = 128;
-#else
   static constexpr int value =
       Point<STENCIL>::R == 1 ? ((C == 2 || K <= 2) ? 168 : 255) : ((C == 2 && K == 1) ? 168 : 255);
-#endif
 };
 
 template <int STENCIL, int NW, int K, int C, bool REDUCE, bool STORE, int RPS = 1>

@@ -15,7 +15,7 @@ from paper_1705_00103_b200 import cjm  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cjm9_4096"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-st, nx, ny, tol, _ = CONFIGS[cfg]
+st, nx, ny, tol = CONFIGS[cfg][:4]
 u0, b, h = make_problem(st, nx, ny, 0, ny)
 ud, bd = torch.from_numpy(u0).cuda(), torch.from_numpy(b).cuda()
 L = cjm.lib()

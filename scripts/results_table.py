@@ -22,7 +22,8 @@ DIGESTS = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_digests.j
 
 
 def run(name, reps=3):
-    st, nx, ny, tol, desc = CONFIGS[name]
+    st, nx, ny, tol = CONFIGS[name][:4]
+    desc = CONFIGS[name][-1]
     r = 2 if st == 17 else 1
     u0, b, h = inputs.test_problem(nx, ny, r)
     bd = torch.from_numpy(b).cuda()

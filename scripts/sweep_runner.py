@@ -19,7 +19,7 @@ from paper_1705_00103_b200 import cjm  # noqa: E402
 
 
 def run(config, count, warm, **kw):
-    st, nx, ny, tol, _ = CONFIGS[config]
+    st, nx, ny, tol = CONFIGS[config][:4]
     u0, b, h = make_problem(st, nx, ny, 0, ny)
     ud, bd = torch.from_numpy(u0).cuda(), torch.from_numpy(b).cuda()
     with cjm.Plan(st, nx, ny, h, tol, **kw) as plan:
@@ -45,7 +45,7 @@ if __name__ == "__main__":
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--temporal-k", type=int, default=0)
     ap.add_argument("--ks", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
-    ap.add_argument("--variants", type=lambda v: [int(x) for x in v.split(",")], default=[3, 4])
+    ap.add_argument("--variants", type=lambda v: [int(x) for x in v.split(",")], default=[3, 7])
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--chunk-rows", type=int, default=0)

@@ -51,6 +51,30 @@ def test_scheduler_bitwise_equals_oracle(stencil, nx, ny):
     assert np.array_equal(s["w"], o["w"])
 
 
+@pytest.mark.parametrize("stencil,nx,ny", [(9, 64, 64), (17, 1024, 1024), (5, 4096, 4096), (9, 16384, 16384)])
+def test_scheduler_lebedev2_bitwise_equals_oracle(stencil, nx, ny):
+    s = cjm.cjm_schedule(stencil, nx, ny, 1e-8, order=cjm.ORDER_LEBEDEV2)
+    o = oracle.schedule(stencil, nx, ny, 1e-8, order="lebedev2")
+    assert s["P"] == o["P"] and s["m_min"] == o["m_min"]
+    assert np.array_equal(s["t"], o["t"]) and np.array_equal(s["w"], o["w"])
+
+
+def test_buffer_layout_and_halo_xfers():
+    """The NCCL exchange's element-level transfers are cjm_halo_plan's rows in
+    the internal layout (whole rows of pitch ld)."""
+    for nx in (1, 37, 4096, 16384):
+        ld, c0 = cjm.cjm_buffer_layout(nx)
+        assert ld % 32 == 0 and ld >= nx + 2 * c0 and c0 == 8
+    for ny, depth, world in [(100, 1, 4), (4096, 4, 8), (16384, 8, 2)]:
+        for rank in range(world):
+            xs, ld = cjm.cjm_halo_xfers(4096, ny, depth, world, rank)
+            msgs = cjm.cjm_halo_plan(ny, depth, world, rank)
+            assert len(xs) == len(msgs)
+            for x, m in zip(xs, msgs):
+                assert x["peer"] == m["peer"] and x["count"] == m["rows"] * ld
+                assert x["send_off"] == m["send_row"] * ld and x["recv_off"] == m["recv_row"] * ld
+
+
 def test_scheduler_ascending_order_option():
     s = cjm.cjm_schedule(9, 64, 64, 1e-8, order=cjm.ORDER_ASCENDING)
     assert np.all(np.diff(s["w"]) > 0)

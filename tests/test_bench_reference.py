@@ -32,3 +32,11 @@ def test_reference_arm_torchrun_two_ranks():
     assert d["cpu_baseline"]["kind"] == "oracle"
     assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    # the measured step time (not a constant) and the GPU arm's config object
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.config_dict("cjm9_1024", 2)
+    assert d["scaling"] == "strong"
+    k = int(d["cpu_baseline"]["sample"].split()[0])
+    assert abs(d["ms_per_step"] / 1e3 - k * 1024 * 1024 / (d["value"] * 1e9)) < 0.5 * d["ms_per_step"] / 1e3
+    assert d["cpu_baseline"]["time_to_tol_extrapolated_s"] > 0

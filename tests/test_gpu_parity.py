@@ -64,11 +64,11 @@ SHAPES = [(8, 8), (64, 64), (100, 37), (257, 300), (513, 70), (1000, 11), (4, 4)
 
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("nx,ny", SHAPES)
-@pytest.mark.parametrize("tile_w,variant", [(256, 3), (512, 3), (0, 4), (0, 5), (0, 6), (0, 7)])
+@pytest.mark.parametrize("tile_w,variant", [(256, 3), (512, 3), (0, 7)])
 def test_one_sweep_bitwise(stencil, nx, ny, tile_w, variant):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=inputs.SEED_BASE + nx + 7 * ny)
-    kw = dict(temporal_k=1) if (stencil == 17 and variant >= 4) else {}
+    kw = dict(temporal_k=1) if variant == 7 else {}
     with cjm.Plan(stencil, nx, ny, h, 1e-8, tile_w=tile_w, variant=variant, **kw) as plan:
         w = oracle_weights(stencil, nx, ny, plan)
         g = oracle.rhs_to_g(stencil, h, b)
@@ -84,14 +84,13 @@ def test_one_sweep_bitwise(stencil, nx, ny, tile_w, variant):
 @pytest.mark.parametrize("nx,ny,count", [(300, 257, 37), (1030, 515, 20), (64, 64, 324),
                                          (9, 700, 13), (520, 6, 11)])
 @pytest.mark.parametrize("temporal_k", (1, 2, 3, 4))
-@pytest.mark.parametrize("variant", (3, 4, 5, 6, 7))
+@pytest.mark.parametrize("variant", (3, 7))
 def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
     """A run of sweeps through the CUDA-graph hot loop (spans several graph
     chunks when count > graph_chunk), K sweeps fused per launch (temporal
-    blocking), every kernel variant, vs the oracle sweep by sweep."""
-    if stencil == 17 and ((variant in (4, 6) and temporal_k > 1) or (variant == 5 and temporal_k > 2)
-                          or (variant == 7 and temporal_k > 3)):
-        pytest.skip("17-point warp-tiled kernels: K=1 (4 columns/lane), K<=2 (variant 5), K<=3 (7)")
+    blocking), both kernels, vs the oracle sweep by sweep."""
+    if stencil == 17 and variant == 7 and temporal_k > 3:
+        pytest.skip("the 17-point warp-tiled kernel runs K <= 3 (K = 4: variant 3)")
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=3)
     with cjm.Plan(stencil, nx, ny, h, 1e-8, graph_chunk=4, temporal_k=temporal_k,
@@ -107,21 +106,22 @@ def test_sweep_segment_bitwise(stencil, nx, ny, count, temporal_k, variant):
 
 
 @pytest.mark.parametrize("stencil", (5, 9, 17))
-@pytest.mark.parametrize("variant,K", [(7, 1), (7, 2), (7, 3), (7, 4), (4, 2), (5, 3), (6, 1)])
+@pytest.mark.parametrize("warps,K", [(0, 1), (0, 2), (0, 3), (0, 4), (11, 4), (5, 3), (7, 2)])
 @pytest.mark.parametrize("chunk_rows", (1, 7, 64))
 @pytest.mark.parametrize("dyn_pct", ("20", "100"))
-def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows, dyn_pct, monkeypatch):
+def test_dynamic_work_items_bitwise(stencil, warps, K, chunk_rows, dyn_pct, monkeypatch):
     """Hot launches whose CTAs take work items of chunk_rows (strip, row)
     units from a device counter (the default last 20% of the units, or all of
     them): same field as the oracle, sweep by sweep."""
-    if stencil == 17 and ((K > 1 and variant in (4, 6)) or (K > 2 and variant == 5) or K > 3):
-        pytest.skip("17-point warp-tiled kernels: K=1 (4 columns/lane), K<=2 (variant 5), K<=3 (7)")
+    if stencil == 17 and (K > 3 or warps == 11):
+        pytest.skip("the 17-point warp-tiled kernel runs K <= 3 with 4, 5 or 7 warps")
+    variant = 7
     monkeypatch.setenv("CJM_DYN_PCT", dyn_pct)
     r = oracle.reach(stencil)
     nx, ny, count = 1030, 515, 9
     u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=17)
     with cjm.Plan(stencil, nx, ny, h, 1e-8, temporal_k=K, variant=variant, chunk_rows=chunk_rows,
-                  resident=-1, graph_chunk=2) as plan:
+                  resident=-1, graph_chunk=2, warps=warps) as plan:
         w = oracle_weights(stencil, nx, ny, plan)
         ud = dev(u0)
         plan.sweeps(dev(b), ud, 2, count)
@@ -137,12 +137,8 @@ def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows, dyn_pct, mo
                                  dict(tile_w=256, stages=32, ctas_per_sm=2, graph_chunk=7, variant=3),
                                  dict(tile_w=512, temporal_k=3, stages=6, variant=3),
                                  dict(tile_w=256, temporal_k=4, ctas_per_sm=4, variant=3),
-                                 dict(variant=4, temporal_k=3, stages=8, ctas_per_sm=1),
-                                 dict(variant=4, temporal_k=1, stages=2),
-                                 dict(variant=5, temporal_k=2, stages=6, ctas_per_sm=3),
-                                 dict(variant=5, temporal_k=4, stages=8),
-                                 dict(variant=6, temporal_k=2, stages=3, ctas_per_sm=1),
-                                 dict(variant=6, temporal_k=4, stages=5),
+                                 dict(variant=7, temporal_k=1, stages=2),
+                                 dict(variant=7, warps=4, temporal_k=4, stages=8, ctas_per_sm=1),
                                  dict(variant=7, temporal_k=3, stages=3),
                                  dict(variant=7, temporal_k=1, stages=8, ctas_per_sm=3),
                                  dict(variant=7, warps=5, temporal_k=4, stages=6),
@@ -152,7 +148,7 @@ def test_dynamic_work_items_bitwise(stencil, variant, K, chunk_rows, dyn_pct, mo
                                  dict(variant=7, temporal_k=4, warps=11),
                                  dict(variant=7, temporal_k=4, warps=11, stages=4, chunk_rows=5),
                                  dict(variant=7, temporal_k=3, chunk_rows=-1),
-                                 dict(variant=4, temporal_k=2, chunk_rows=100, ctas_per_sm=1)])
+                                 dict(variant=7, temporal_k=2, chunk_rows=100, ctas_per_sm=1)])
 def test_launch_configuration_does_not_change_result(cfg):
     nx, ny = 777, 301
     u0, b, h = inputs.test_problem(nx, ny, 1, init="random", seed=5)
@@ -181,15 +177,12 @@ def test_residual_matches_oracle(stencil):  # noqa: D103
 # ------------------------------------------------------------ full solves
 @pytest.mark.parametrize("stencil", (5, 9, 17))
 @pytest.mark.parametrize("n,init", [(64, "zero"), (64, "random"), (200, "zero"), (129, "random")])
-@pytest.mark.parametrize("temporal_k,variant,resident", [(1, 4, -1), (2, 4, -1), (2, 3, -1), (4, 3, -1),
-                                                          (3, 0, -1), (0, 0, 1), (2, 5, -1), (2, 6, -1),
-                                                          (3, 7, -1)])
+@pytest.mark.parametrize("temporal_k,variant,resident", [(1, 7, -1), (2, 7, -1), (2, 3, -1), (4, 3, -1),
+                                                          (3, 0, -1), (0, 0, 1), (3, 7, -1), (4, 0, -1)])
 def test_solve_matches_oracle(stencil, n, init, temporal_k, variant, resident):
     r = oracle.reach(stencil)
     u0, b, h = inputs.test_problem(n, n, r, init=init)
     uo, ro = oracle.solve(stencil, h, 1e-8, b, u0)
-    if stencil == 17 and variant >= 4 and temporal_k > 1:
-        variant = {4: 0, 5: 5 if temporal_k <= 2 else 0, 6: 0, 7: 7 if temporal_k <= 3 else 0}[variant]
     with cjm.Plan(stencil, n, n, h, 1e-8, temporal_k=temporal_k, variant=variant,
                   resident=resident) as plan:
         assert plan.info()["resident"] == (1 if resident == 1 else 0)
@@ -263,12 +256,13 @@ def test_jacobi_method_matches_oracle_sweeps():
 
 def test_too_deep_ring_is_invalid_arg():
     with pytest.raises(cjm.CJMError) as e:
-        cjm.Plan(9, 4096, 4096, 1 / 4097, 1e-8, stages=32, variant=4)
+        cjm.Plan(9, 4096, 4096, 1 / 4097, 1e-8, stages=32, variant=7, warps=4)
     assert e.value.name == "CJM_ERR_INVALID_ARG"
 
 
-@pytest.mark.parametrize("kw", [dict(variant=7, warps=6), dict(variant=4, warps=5), dict(warps=-1),
-                                dict(variant=7, temporal_k=3, warps=11),
+@pytest.mark.parametrize("kw", [dict(variant=7, warps=6), dict(variant=3, warps=5), dict(warps=-1),
+                                dict(variant=7, temporal_k=3, warps=11), dict(variant=4),
+                                dict(variant=5), dict(variant=6),
                                 dict(variant=8), dict(variant=7, temporal_k=5),
                                 dict(variant=7, temporal_k=4, stages=2)])
 def test_invalid_launch_options_are_invalid_arg(kw):
@@ -325,14 +319,22 @@ def test_bad_pitch_is_invalid_arg():
 
 # ------------------------------------------------------------ stored oracle solves
 def _digest_cases():
+    """(name, temporal_k, resident): every stored case in the default launch
+    configuration (the one bench.py times); those up to 8192^2 also with K = 1
+    and K = 2 (the 16384^2 target takes ~30 s per solve in the default one)."""
     if not os.path.exists(DIGESTS):
         return []
     with open(DIGESTS) as f:
-        return sorted(json.load(f).keys())
+        recs = json.load(f)
+    out = []
+    for name in sorted(recs):
+        out.append((name, 0, 0))
+        if recs[name]["nx"] * recs[name]["ny"] <= 8192 * 8192:
+            out += [(name, 1, -1), (name, 2, -1)]
+    return out
 
 
-@pytest.mark.parametrize("name", _digest_cases())
-@pytest.mark.parametrize("temporal_k,resident", [(1, -1), (2, -1), (0, 0)])
+@pytest.mark.parametrize("name,temporal_k,resident", _digest_cases())
 def test_solve_matches_stored_oracle_digest(name, temporal_k, resident):  # noqa: D103
     """Full solves at BASELINE sizes vs the oracle's stored result
     (tests/make_oracle_digests.py): same iterations, sampled nodes within
@@ -341,8 +343,7 @@ def test_solve_matches_stored_oracle_digest(name, temporal_k, resident):  # noqa
         rec = json.load(f)[name]
     st, nx, ny, h, tol = rec["stencil"], rec["nx"], rec["ny"], rec["h"], rec["tol"]
     free = torch.cuda.mem_get_info()[0]
-    if free < 9 * (nx + 4) * (ny + 4) * 8:
-        pytest.skip("not enough device memory")
+    assert free >= 9 * (nx + 4) * (ny + 4) * 8, "a B200 holds every stored case"
     r = oracle.reach(st)
     u0, b, h2 = inputs.test_problem(nx, ny, r, init=rec["init"])
     assert h2 == h
@@ -444,6 +445,75 @@ def test_resident_segment_bitwise(stencil, nx, ny, count):
         g = oracle.rhs_to_g(stencil, h, b)
         want = oracle.sweeps(stencil, u0, g, w, 3, count)
         assert_field_parity(host(ud), want, r)
+
+
+@pytest.mark.parametrize("nx,ny,resident", [(2048, 4, 0), (2048, 4, 1), (1500, 5, 0), (2600, 4, 1)])
+def test_resident_17_point_thin_slabs(nx, ny, resident):
+    """17-point grids only a few rows high: every resident CTA slab but the
+    last must own >= r = 2 rows (it publishes its first / last r rows to its
+    neighbours); bitwise vs the oracle."""
+    r = 2
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=37)
+    with cjm.Plan(17, nx, ny, h, 1e-8, resident=resident) as plan:
+        w = oracle_weights(17, nx, ny, plan)
+        ud = dev(u0)
+        plan.sweeps(dev(b), ud, 1, 24)
+    want = oracle.sweeps(17, u0, oracle.rhs_to_g(17, h, b), w, 1, 24)
+    assert_field_parity(host(ud), want, r)
+
+
+# ------------------------------------------------------------ cycles shorter than K (check launch)
+@pytest.mark.parametrize("stencil,n,tol", [(9, 4, 0.5), (5, 5, 0.6), (17, 5, 0.7)])
+def test_cycle_shorter_than_temporal_k(stencil, n, tol):
+    """P < K: the check launch runs one sweep (a configured launch), the rest
+    of the cycle the hot path; same iterations and field as the oracle."""
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(n, n, r, init="random", seed=43)
+    K = 3 if stencil == 17 else 4
+    s = oracle.schedule(stencil, n, n, tol)
+    assert s["P"] < K
+    uo, ro = oracle.solve(stencil, h, tol, b, u0)
+    with cjm.Plan(stencil, n, n, h, tol, temporal_k=K, resident=-1) as plan:
+        assert plan.P == s["P"]
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud, ok=(0, 3, 5))
+    assert rep["status"][len("CJM_"):].replace("ERR_", "") == ro["status"]
+    assert rep["iterations"] == ro["iterations"]
+    assert_field_parity(host(ud), uo, r)
+
+
+@pytest.mark.parametrize("check", (2, 3, 5))
+def test_jacobi_check_interval_shorter_than_temporal_k(check):
+    """Classical Jacobi (w = 1) checked every 2 / 3 / 5 sweeps with K = 4
+    fused sweeps per hot launch: the oracle's Jacobi sweeps, bitwise."""
+    n, cycles = 300, 4
+    u0, b, h = inputs.test_problem(n, n, 1, init="random", seed=47)
+    with cjm.Plan(9, n, n, h, 1e-8, method=cjm.METHOD_JACOBI, jacobi_check=check, temporal_k=4,
+                  max_cycles=cycles, resident=-1) as plan:
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud, ok=(3,))
+    assert rep["status"] == "CJM_ERR_NOT_CONVERGED" and rep["iterations"] == cycles * check
+    want = oracle.sweeps(9, u0, oracle.rhs_to_g(9, h, b), np.ones(check), 0, cycles * check)
+    assert_field_parity(host(ud), want, 1)
+
+
+# ------------------------------------------------------------ power-of-two ordering
+@pytest.mark.parametrize("stencil,n", [(9, 200), (17, 129), (5, 300)])
+def test_lebedev2_order_solve_matches_oracle(stencil, n):
+    """CJM_ORDER_LEBEDEV2 (P = 2^a, classical Lebedev-Finogenov order): the
+    plan's weights equal the oracle's power-of-two schedule and the solve
+    equals the oracle's solve with those weights, bitwise."""
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(n, n, r, init="random", seed=53)
+    s = oracle.schedule(stencil, n, n, 1e-8, order="lebedev2")
+    uo, ro = oracle.solve(stencil, h, 1e-8, b, u0, weights_override=s["w"])
+    with cjm.Plan(stencil, n, n, h, 1e-8, order=cjm.ORDER_LEBEDEV2) as plan:
+        assert plan.P == s["P"] and np.array_equal(plan.info()["weights"], s["w"])
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud)
+    assert rep["status"] == "CJM_OK" and ro["status"] == "OK"
+    assert rep["iterations"] == ro["iterations"]
+    assert_field_parity(host(ud), uo, r)
 
 
 @pytest.mark.gpu

@@ -7,6 +7,12 @@ function its NCCL exchange uses) lays them out, sweeps its slab with the
 oracle and allreduces (sum, max) of the per-slab reduction.  The gathered
 field must be bitwise equal to the single-domain oracle, and the allreduced
 norms must match the single-domain ones.
+
+test_library_transfer_list_deep_halos runs the library's K-fused multi-GPU
+schedule itself with gloo as the transport: host buffers in the library's
+internal layout (cjm_buffer_layout), the exact transfers its NCCL exchange
+issues (cjm_halo_xfers: peers, element offsets, counts; the g rows once per
+solve, the u rows after every K-sweep launch), H = K r deep halos.
 """
 from __future__ import annotations
 
@@ -130,3 +136,104 @@ def test_halo_plan_geometry():
                 assert y0 + m["send_row"] - r == py0 + pm["recv_row"] - r
     with pytest.raises(cjm.CJMError):
         cjm.cjm_halo_plan(8, 2, 4, 0)    # slabs of 2 rows < 2r+1
+
+
+# ----------------------------------------------------------------------------
+# The library's own transfer list on gloo: deep halos of K-fused launches
+# ----------------------------------------------------------------------------
+
+def _xfer_worker(rank, world, port, stencil, nx, ny, K, nlaunch, out):
+    """One rank of the K-fused multi-GPU schedule, with the device buffers
+    replaced by flat host buffers in the library's internal layout
+    (cjm_buffer_layout) and the NCCL exchange replaced by gloo send / recv of
+    exactly the transfers the library issues (cjm_halo_xfers: peer, element
+    offsets, counts).  The K sweeps of a launch are the oracle's sweeps on the
+    slab extended by its H = K r ghost rows (the rows inside the global grid
+    computed redundantly, as the kernel does)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r = oracle.reach(stencil)
+        H = K * r
+        u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=19)
+        s = oracle.schedule(stencil, nx, ny, 1e-8)
+        g_all = oracle.rhs_to_g(stencil, h, b)
+        y0, nyl = cjm.cjm_slab(ny, world, rank)
+        ld, c0 = cjm.cjm_buffer_layout(nx)
+        xs, ld2 = cjm.cjm_halo_xfers(nx, ny, H, world, rank)
+        assert ld2 == ld
+        rows = nyl + 2 * H
+        ubuf = np.zeros(rows * ld)
+        gbuf = np.zeros(rows * ld)
+        U, G = ubuf.reshape(rows, ld), gbuf.reshape(rows, ld)
+        cols = slice(c0 - r, c0 + nx + r)
+        # global row y (ghost rows -r..-1 and ny..ny+r-1) <-> u0 row y + r
+        lo_g, hi_g = max(-r, y0 - H), min(ny + r, y0 + nyl + H)   # rows that exist globally
+        for y in range(lo_g, hi_g):
+            U[y - y0 + H, cols] = u0[y + r]
+        for y in range(y0, y0 + nyl):                            # g: my interior rows only
+            G[y - y0 + H, c0:c0 + nx] = g_all[y]
+
+        def exchange(buf):
+            reqs, recvs = [], []
+            for x in xs:
+                send = torch.from_numpy(buf[x["send_off"]:x["send_off"] + x["count"]].copy())
+                recv = torch.empty(x["count"], dtype=torch.float64)
+                reqs += [dist.isend(send, x["peer"]), dist.irecv(recv, x["peer"])]
+                recvs.append((x, recv))
+            for q in reqs:
+                q.wait()
+            for x, recv in recvs:
+                buf[x["recv_off"]:x["recv_off"] + x["count"]] = recv.numpy()
+
+        exchange(gbuf)                    # once per solve: the neighbours' g rows
+        exchange(ubuf)                    # u_0's halo
+        a, e = lo_g - y0 + H, hi_g - y0 + H   # local rows of the extended slab
+        norms = []
+        for k in range(nlaunch):
+            ext = U[a:e, cols].copy()     # outermost r rows act as fixed ghosts
+            gext = G[a + r:e - r, c0:c0 + nx]
+            if k == 0:
+                ss, mm = oracle.delta_norms(stencil, U[H - r:H + nyl + r, cols],
+                                            G[H:H + nyl, c0:c0 + nx])
+                t = torch.tensor([ss, mm], dtype=torch.float64)
+                dist.all_reduce(t[:1], op=dist.ReduceOp.SUM)
+                dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
+                norms.append((t[0].item(), t[1].item()))
+            for l in range(K):
+                ext = oracle.sweep(stencil, ext, gext, s["w"][(k * K + l) % s["P"]])
+            U[H:H + nyl, cols] = ext[H - a:H - a + nyl]
+            exchange(ubuf)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (y0, U[H:H + nyl, cols].copy()))
+        if rank == 0:
+            out.put((gathered, norms))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,stencil,nx,ny,K", [(2, 9, 37, 50, 4), (3, 17, 23, 61, 3),
+                                                   (2, 5, 30, 29, 2), (4, 9, 19, 60, 1)])
+def test_library_transfer_list_deep_halos(world, stencil, nx, ny, K):
+    nlaunch = 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xfer_worker, args=(rk, world, port, stencil, nx, ny, K, nlaunch, q))
+             for rk in range(world)]
+    for p in procs:
+        p.start()
+    gathered, norms = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    r = oracle.reach(stencil)
+    u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=19)
+    s = oracle.schedule(stencil, nx, ny, 1e-8)
+    g = oracle.rhs_to_g(stencil, h, b)
+    ss, mm = oracle.delta_norms(stencil, u0, g)
+    assert norms[0][0] == pytest.approx(ss, rel=1e-13) and norms[0][1] == mm
+    want = oracle.sweeps(stencil, u0, g, s["w"], 0, nlaunch * K)
+    field = np.concatenate([blk for _, blk in sorted(gathered, key=lambda t: t[0])])
+    assert np.array_equal(field, want[r:r + ny])

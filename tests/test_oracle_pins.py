@@ -450,3 +450,54 @@ def test_sweeps_segment_equals_repeated_sweep():
     for k in range(11):
         u = oracle.sweep(17, u, g, s["w"][(s["P"] - 4 + k) % s["P"]])
     assert np.array_equal(oracle.sweeps(17, u0, g, s["w"], s["P"] - 4, 11), u)
+
+
+# ----------------------------------------------------------------------------
+# Power-of-two ordering (order option LEBEDEV2, DESIGN R3)
+# ----------------------------------------------------------------------------
+
+def test_cycle_len_pow2_is_smallest_power_of_two():
+    for m in list(range(1, 300)) + [5092, 20353, 81396, 199371]:
+        P, a = oracle.cycle_len_pow2(m)
+        assert P == 2 ** a and P >= m and (P == 1 or P // 2 < m)
+
+
+def test_lebedev2_theta8_is_the_classical_ordering():
+    """For P = 8 the power-of-two recursion gives the Lebedev-Finogenov
+    theta_8 = (1, 15, 7, 9, 3, 13, 5, 11) of zero indices 2i-1 (the classical
+    stable ordering the generalised 2^a 3^b one reduces to when b = 0)."""
+    s = oracle.schedule(9, 6, 6, 0.3, order="lebedev2")
+    assert s["P"] >= s["m_min"] and s["b"] == 0
+    assert list(oracle.ordering(3, 0)) == [1, 15, 7, 9, 3, 13, 5, 11]
+
+
+@pytest.mark.parametrize("stencil,n,tol", [(9, 64, 1e-8), (17, 40, 1e-6), (5, 100, 1e-10)])
+def test_lebedev2_weights_product_identity_and_stability(stencil, n, tol):
+    """The LEBEDEV2 weights are the reciprocals of the mapped zeros of T_P,
+    P = 2^a (closed-form T_P identity), and the suffix amplification of the
+    order stays <= 1."""
+    s = oracle.schedule(stencil, n, n, tol, order="lebedev2")
+    kmin, kmax, P, w = s["kappa_min"], s["kappa_max"], s["P"], s["w"]
+    assert P == 2 ** s["a"] and P // 2 < s["m_min"] <= P
+    assert sorted(s["t"].tolist()) == list(range(1, 2 * P, 2))
+    kap = np.concatenate([np.linspace(kmin, kmax, 2001), np.geomspace(kmin, kmax, 501)])
+    prod = np.ones_like(kap)
+    for wk in w:
+        prod *= 1.0 - wk * kap
+    mu = (kmax + kmin) / (kmax - kmin)
+    ref = _cheb_T(P, (kmax + kmin - 2 * kap) / (kmax - kmin)) / _cheb_T(P, np.array([mu]))[0]
+    bound = 1.0 / _cheb_T(P, np.array([mu]))[0]
+    assert np.max(np.abs(prod - ref)) <= 1e-8 * bound
+    logabs = np.log(np.abs(1.0 - np.outer(w, kap[::5])))
+    assert np.exp(np.cumsum(logabs[::-1], axis=0).max()) <= 1.0 + 1e-6
+
+
+def test_lebedev2_solve_converges_like_lebedev23():
+    """A solve with the LEBEDEV2 weights (weights_override) reaches the same
+    tolerance in one cycle of its (longer) power-of-two length."""
+    n = 63
+    u0, b, h = inputs.test_problem(n, n, 1)
+    s2 = oracle.schedule(9, n, n, 1e-8, order="lebedev2")
+    u, rep = oracle.solve(9, h, 1e-8, b, u0, weights_override=s2["w"])
+    assert rep["status"] == "OK" and rep["cycles"] == 1 and rep["iterations"] == s2["P"]
+    assert rep["r_l2"] <= 1e-8 * rep["r0_l2"]
