@@ -102,6 +102,17 @@ typedef enum {
  * check interval of jacobi_check sweeps and it has no stagnation test. */
 typedef enum { CJM_METHOD_CHEBYSHEV = 0, CJM_METHOD_JACOBI = 1 } cjm_method;
 
+/* Outer ghost ring of the 17-point stencil (reach 2).  DIRICHLET: the
+ * caller's data in both rings, never written (the test problem's analytic
+ * values; the closed-form kappa_min^(17) is then a lower bound of
+ * lambda_min, DESIGN R2).  ODD: the outer ring is set by odd reflection
+ * through the boundary, u(mirror) = 2 u_b - u (the boundary ring u_b is the
+ * Dirichlet data), recomputed from the iterate before every sweep and every
+ * residual: the iteration operator is then the odd extension whose
+ * lambda_min the closed form P:126-134 gives exactly (DESIGN R12, SURVEY
+ * [V2]). */
+typedef enum { CJM_CLOSURE_DIRICHLET = 0, CJM_CLOSURE_ODD = 1 } cjm_closure;
+
 typedef struct {
     int max_cycles;        /* default 8 (Jacobi: default 100000) */
     int order;             /* cjm_order, default CJM_ORDER_LEBEDEV23 */
@@ -151,6 +162,11 @@ typedef struct {
                               (5/9-point at temporal_k 4: one CTA per SM); 0 = the
                               count that keeps the most consumer warps resident per
                               SM */
+    int closure;           /* cjm_closure, default DIRICHLET.  ODD: 17-point only,
+                              single GPU, one sweep per launch (temporal_k 0 or 1),
+                              no resident kernel; else INVALID_ARG.  The caller's
+                              outer ring is read but never written (the library
+                              reflects into its own buffers). */
     int chunk_rows;        /* warp-tiled kernel, non-reducing launches: every CTA
                               streams a static range of 80% of its share of the
                               (strip, row) units, the last 20% go out in work items of

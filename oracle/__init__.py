@@ -82,9 +82,11 @@ def lib():
         L.oracle_residual.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, dp, C.c_long,
                                       dp, C.c_long, dp, dp]
         L.oracle_solve.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
-                                   dp, C.c_long, dp, C.c_long, dp, C.c_long, C.POINTER(Report)]
+                                   dp, C.c_long, dp, C.c_long, dp, C.c_long, C.POINTER(Report),
+                                   C.c_int]
         L.oracle_sweeps.argtypes = [C.c_int, C.c_int, C.c_int, dp, C.c_long, dp, C.c_long, dp,
-                                    C.c_long, C.c_long, C.c_long]
+                                    C.c_long, C.c_long, C.c_long, C.c_int]
+        L.oracle_odd_closure.argtypes = [C.c_int, C.c_int, dp, C.c_long]
         L.oracle_mask_sweep.argtypes = [C.c_int, C.c_int, dp, C.c_long, dp, dp, dp, dp, dp, C.c_long,
                                         dp, C.c_long, C.c_double, dp, C.c_long]
         L.oracle_mask_residual.argtypes = [C.c_int, C.c_int, dp, C.c_long, dp, dp, dp, dp, dp, C.c_long,
@@ -193,16 +195,31 @@ def sweep(stencil: int, u: np.ndarray, g: np.ndarray, w: float) -> np.ndarray:
     return out
 
 
+CLOSURES = {"dirichlet": 0, "odd": 1}
+
+
+def odd_closure(u: np.ndarray) -> np.ndarray:
+    """A copy of the 17-point field u (2 ghost rings) with its outer ring set
+    by odd reflection through the boundary (oracle_odd_closure, DESIGN R12)."""
+    out = np.array(u, dtype=np.float64, order="C", copy=True)
+    ny, nx = out.shape[0] - 4, out.shape[1] - 4
+    lib().oracle_odd_closure(nx, ny, _dp(out), out.shape[1])
+    return out
+
+
 def sweeps(stencil: int, u: np.ndarray, g: np.ndarray, w: np.ndarray, first: int,
-           count: int) -> np.ndarray:
-    """`count` scheduled sweeps (weight w[(first+k) mod P] at sweep k)."""
+           count: int, closure: str = "dirichlet") -> np.ndarray:
+    """`count` scheduled sweeps (weight w[(first+k) mod P] at sweep k);
+    closure="odd" (17-point): outer ghost ring reflected before every sweep."""
     r = reach(stencil)
     out = np.array(u, dtype=np.float64, order="C", copy=True)
     g = np.ascontiguousarray(g, dtype=np.float64)
     w = np.ascontiguousarray(w, dtype=np.float64)
     ny, nx = out.shape[0] - 2 * r, out.shape[1] - 2 * r
-    lib().oracle_sweeps(stencil, nx, ny, _dp(out), out.shape[1], _dp(g), nx, _dp(w), len(w),
-                        first, count)
+    st = lib().oracle_sweeps(stencil, nx, ny, _dp(out), out.shape[1], _dp(g), nx, _dp(w), len(w),
+                             first, count, CLOSURES[closure])
+    if st != 0:
+        raise ValueError(f"oracle_sweeps: status {st}")
     return out
 
 
@@ -228,8 +245,11 @@ def residual(stencil: int, h: float, b: np.ndarray, u: np.ndarray) -> tuple[floa
 
 
 def solve(stencil: int, h: float, tol: float, b: np.ndarray, u0: np.ndarray,
-          max_cycles: int = 8, weights_override: np.ndarray | None = None):
-    """Full CJM solve.  Returns (u, report dict); u0 is not modified."""
+          max_cycles: int = 8, weights_override: np.ndarray | None = None,
+          closure: str = "dirichlet"):
+    """Full CJM solve.  Returns (u, report dict); u0 is not modified.
+    closure="odd" (17-point): the outer ghost ring by odd reflection,
+    recomputed before every sweep and residual (DESIGN R12)."""
     u = np.array(u0, dtype=np.float64, order="C", copy=True)
     b = np.ascontiguousarray(b, dtype=np.float64)
     ny, nx = b.shape
@@ -240,7 +260,7 @@ def solve(stencil: int, h: float, tol: float, b: np.ndarray, u0: np.ndarray,
     else:
         wo, wp, wl = None, None, 0
     lib().oracle_solve(stencil, nx, ny, h, tol, max_cycles, _dp(b), nx, _dp(u), u.shape[1],
-                       wp, wl, C.byref(rep))
+                       wp, wl, C.byref(rep), CLOSURES[closure])
     return u, rep.as_dict()
 
 

@@ -32,6 +32,9 @@
  *   5. residual norm at cycle boundaries,         P:459-460 "until reaching a
  *      stop when ||r||_2 <= tol ||r_0||_2         prescribed tolerance";
  *                                                 DESIGN R4
+ *   option: 17-point outer ghost ring by odd     P:126-134 (the closed-form
+ *      reflection (oracle_odd_closure)            kappa_min^(17) is exact for
+ *                                                 it); DESIGN R12
  *
  * Grid convention (DESIGN R1): nx, ny = interior unknowns; the paper's
  * N_x = nx+1, N_y = ny+1 mesh intervals; node (i,j), 1<=i<=nx, 1<=j<=ny; r
@@ -336,21 +339,50 @@ void oracle_residual(int stencil, int nx, int ny, double h,
     free(g);
 }
 
+/* 17-point closure option (NEXT-4; DESIGN R12): the outer ghost ring by odd
+ * reflection through the boundary instead of given data.  With homogeneous
+ * Dirichlet data the 17-point operator then is the odd extension whose
+ * smallest eigenvalue the closed form kappa_min^(17) of P:126-134 gives
+ * EXACTLY (SURVEY [V2]); with data u_b on the boundary nodes the reflection
+ * is affine, u(mirror of i) = 2 u_b - u(i), exact for fields linear across
+ * the boundary.  0-based interior (i, j), boundary nodes i = -1, nx and
+ * j = -1, ny, outer ring i = -2, nx+1 and j = -2, ny+1; u has r = 2 ghost
+ * rings.  Columns first (rows -1..ny), then rows (every column, so the
+ * corners of the outer ring reflect the reflected columns):
+ *   u(-2, j) = 2 u(-1, j) - u(0, j),   u(nx+1, j) = 2 u(nx, j) - u(nx-1, j)
+ *   u(i, -2) = 2 u(i, -1) - u(i, 0),   u(i, ny+1) = 2 u(i, ny) - u(i, ny-1)
+ * each as (2.0 * a) - b (2a exact, one rounding). */
+void oracle_odd_closure(int nx, int ny, double *u, long ldu)
+{
+#define U_(i, j) u[(long)((j) + 2) * ldu + ((i) + 2)]
+    for (int j = -1; j <= ny; j++) {
+        U_(-2, j) = 2.0 * U_(-1, j) - U_(0, j);
+        U_(nx + 1, j) = 2.0 * U_(nx, j) - U_(nx - 1, j);
+    }
+    for (int i = -2; i <= nx + 1; i++) {
+        U_(i, -2) = 2.0 * U_(i, -1) - U_(i, 0);
+        U_(i, ny + 1) = 2.0 * U_(i, ny) - U_(i, ny - 1);
+    }
+#undef U_
+}
+
 /* `count` consecutive sweeps of the schedule (weight w[(first + k) mod P] at
  * sweep k), double buffered exactly as in oracle_solve; u is overwritten with
  * the result.  Used for fixed segments of a solve at sizes where the whole
  * solve would take the oracle too long. */
 int oracle_sweeps(int stencil, int nx, int ny, double *u, long ldu,
                   const double *g, long ldg, const double *w, long P,
-                  long first, long count)
+                  long first, long count, int closure)
 {
     int r = oracle_reach(stencil);
+    if (closure && stencil != 17) return OR_INVALID;
     long rows = ny + 2 * r;
     double *v = (double *)malloc(sizeof(double) * (size_t)rows * ldu);
     if (!v) return OR_OOM;
     memcpy(v, u, sizeof(double) * (size_t)rows * ldu);
     double *cur = u, *nxt = v;
     for (long k = 0; k < count; k++) {
+        if (closure) oracle_odd_closure(nx, ny, cur, ldu);
         oracle_sweep(stencil, nx, ny, cur, ldu, g, ldg, w[(first + k) % P], nxt, ldu);
         double *tmp = cur; cur = nxt; nxt = tmp;
     }
@@ -377,16 +409,18 @@ typedef struct {
  * -> STAGNATED (fp64 floor); max_cycles reached -> NOT_CONVERGED.  u then
  * holds the last cycle-boundary iterate.
  * weights_override (may be NULL): run these P weights instead (tests only:
- * e.g. another ordering of the same set). */
+ * e.g. another ordering of the same set).
+ * closure = 1 (17-point only): the outer ghost ring by odd reflection,
+ * recomputed from the iterate before every sweep and every residual. */
 int oracle_solve(int stencil, int nx, int ny, double h, double tol,
                  int max_cycles, const double *b, long ldb, double *u, long ldu,
                  const double *weights_override, long override_len,
-                 oracle_report *rep)
+                 oracle_report *rep, int closure)
 {
     memset(rep, 0, sizeof(*rep));
     int r = oracle_reach(stencil);
     if (!r || nx < 4 || ny < 4 || !(h > 0.0) || !(tol > 0.0 && tol < 1.0)
-        || max_cycles < 1)
+        || max_cycles < 1 || (closure && stencil != 17))
         return rep->status = OR_INVALID;
 
     double kmin, kmax;
@@ -422,6 +456,7 @@ int oracle_solve(int stencil, int nx, int ny, double h, double tol,
 
     double sc = fabs(oracle_gscale(stencil, h));
     double s, mx;
+    if (closure) oracle_odd_closure(nx, ny, u, ldu);
     oracle_delta_norms(stencil, nx, ny, u, ldu, g, ldg, &s, &mx);
     rep->r0_l2 = sqrt(s) / sc;
     rep->r0_linf = mx / sc;
@@ -437,11 +472,13 @@ int oracle_solve(int stencil, int nx, int ny, double h, double tol,
     int status = OR_NOT_CONVERGED;
     for (int c = 1; c <= max_cycles; c++) {
         for (long k = 0; k < P; k++) {
+            if (closure) oracle_odd_closure(nx, ny, cur, ldu);
             oracle_sweep(stencil, nx, ny, cur, ldu, g, ldg, w[k], nxt, ldu);
             double *tmp = cur; cur = nxt; nxt = tmp;
         }
         rep->iterations += P;
         rep->cycles = c;
+        if (closure) oracle_odd_closure(nx, ny, cur, ldu);
         oracle_delta_norms(stencil, nx, ny, cur, ldu, g, ldg, &s, &mx);
         double rho = sqrt(s) / sc;
         rep->r_l2 = rho;

@@ -27,6 +27,7 @@ STENCIL_MASK, STENCIL_5, STENCIL_9, STENCIL_17 = 1, 5, 9, 17
 BC_DIRICHLET = 0
 ORDER_LEBEDEV23, ORDER_ASCENDING, ORDER_LEBEDEV2 = 0, 1, 2
 METHOD_CHEBYSHEV, METHOD_JACOBI = 0, 1
+CLOSURE_DIRICHLET, CLOSURE_ODD = 0, 1
 
 STATUS = {0: "CJM_OK", 1: "CJM_ERR_INVALID_ARG", 2: "CJM_ERR_UNSUPPORTED",
           3: "CJM_ERR_NOT_CONVERGED", 4: "CJM_ERR_DIVERGED", 5: "CJM_ERR_STAGNATED",
@@ -56,7 +57,7 @@ class Options(C.Structure):
                 ("tile_w", C.c_int),
                 ("ctas_per_sm", C.c_int), ("stages", C.c_int), ("graph_chunk", C.c_int),
                 ("resident", C.c_int), ("band_split", C.c_int), ("warps", C.c_int),
-                ("chunk_rows", C.c_int)]
+                ("closure", C.c_int), ("chunk_rows", C.c_int)]
 
 
 class HaloMsg(C.Structure):

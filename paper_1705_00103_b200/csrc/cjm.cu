@@ -64,6 +64,45 @@ __global__ void cjm_scale_kernel(double* g, long long ld, int nx, int rows, doub
   }
 }
 
+// 17-point odd-reflection closure (cjm_options.closure, DESIGN R12): the
+// outer ghost ring of the INPUT iterate (buffer state->cur) from the boundary
+// nodes and the interior, before every sweep.  0-based interior (i, j) at
+// row j + H, column PADL + i; boundary i = -1, nx / j = -1, ny; outer ring
+// i = -2, nx+1 / j = -2, ny+1.  Columns (rows -1..ny) first, then rows (all
+// columns; the four outer corners reflect the reflected columns, recomputed
+// inline with the same operations):  u(mirror) = (2 u_b) - u, 2 u_b exact.
+__global__ void cjm_odd_closure_kernel(double* buf0, double* buf1, const SweepState* st,
+                                       long long ld, int H, int nx, int ny) {
+  double* u = (__ldcg(&st->cur) & 1u) ? buf1 : buf0;
+  auto at = [&](int i, int j) -> double& { return u[(long long)(j + H) * ld + PADL + i]; };
+  auto refl = [](double ub, double v) { return __dsub_rn(__dmul_rn(2.0, ub), v); };
+  const int ncol = ny + 2;            // column phase: rows -1..ny, both sides
+  const int nrow = nx + 4;            // row phase: columns -2..nx+1, both sides
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * (ncol + nrow); t += gridDim.x * blockDim.x) {
+    if (t < 2 * ncol) {
+      const int j = t / 2 - 1;
+      if (t & 1) at(nx + 1, j) = refl(at(nx, j), at(nx - 1, j));
+      else at(-2, j) = refl(at(-1, j), at(0, j));
+    } else {
+      const int q = t - 2 * ncol, i = q / 2 - 2;
+      const bool bot = q & 1;
+      const int jb = bot ? ny : -1, jm = bot ? ny - 1 : 0, jo = bot ? ny + 1 : -2;
+      double ub, v;
+      if (i == -2) {                  // corner: the column reflection of rows jb and jm
+        ub = refl(at(-1, jb), at(0, jb));
+        v = refl(at(-1, jm), at(0, jm));
+      } else if (i == nx + 1) {
+        ub = refl(at(nx, jb), at(nx - 1, jb));
+        v = refl(at(nx, jm), at(nx - 1, jm));
+      } else {
+        ub = at(i, jb);
+        v = at(i, jm);
+      }
+      at(i, jo) = refl(ub, v);
+    }
+  }
+}
+
 }  // namespace cjm
 
 namespace {
@@ -212,6 +251,7 @@ struct cjm_plan_s {
                         // (0: static ranges, -1: chosen per launch)
   int dyn_pct = 20;     // percent of the units scheduled dynamically (CJM_DYN_PCT)
   int band_split = 0;  // split hot sweeps into boundary / interior bands even without NCCL
+  int closure = CJM_CLOSURE_DIRICHLET;   // 17-point outer ghost ring (DESIGN R12)
   // resident (whole grid in shared memory) hot path
   int resident = 0, res_ctas = 0, res_rows = 0;
   size_t res_smem = 0;
@@ -316,6 +356,13 @@ switch (pl->mask_r) {
 cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int row0 = 0,
                         int nrows = -1, int advance = 1) {
   if (pl->stencil == CJM_STENCIL_MASK) return launch_mask(pl, mode, st);   // K = 1, one band
+  if (pl->closure == CJM_CLOSURE_ODD) {   // K = 1, one band, one GPU: reflect the input's outer ring
+    const int n = 2 * (pl->ny + 2) + 2 * (pl->nx + 4);
+    cjm::cjm_odd_closure_kernel<<<(n + 255) / 256, 256, 0, st>>>(pl->buf[0], pl->buf[1], pl->state,
+                                                                 pl->ld, pl->H, pl->nx, pl->ny);
+    CUDA_TRY(cudaGetLastError());
+    pl->launches += 1;
+  }
   if (nrows < 0) nrows = pl->ny_local;
   cjm::SweepParams sp;
   sp.buf[0] = pl->buf[0];
@@ -931,8 +978,14 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
       opt.temporal_k < 0 || opt.temporal_k > 4 ||
       (opt.variant != 0 && opt.variant != 3 && opt.variant != 7) ||
       opt.stages > 32 || opt.ctas_per_sm < 0 || opt.graph_chunk < 0 || opt.max_cycles < 0 ||
-      opt.jacobi_check < 0) {
+      opt.jacobi_check < 0 || (opt.closure != CJM_CLOSURE_DIRICHLET && opt.closure != CJM_CLOSURE_ODD)) {
     set_error("cjm_plan", "invalid argument");
+    return CJM_ERR_INVALID_ARG;
+  }
+  if (opt.closure == CJM_CLOSURE_ODD &&
+      (stencil != CJM_STENCIL_17 || opt.world_size != 1 || opt.nccl_id || opt.temporal_k > 1 ||
+       opt.resident == 1 || opt.band_split)) {
+    set_error("cjm_plan", "closure=ODD: 17-point, single GPU, temporal_k 1, no resident kernel");
     return CJM_ERR_INVALID_ARG;
   }
   int y0 = 0, nyl = 0;
@@ -956,6 +1009,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   pl->gscale = mask ? -1.0 : stencil == 5 ? -(h * h) * 0.25 : stencil == 9 ? -(h * h) * 0.3
                                                                       : -(h * h) * (72.0 / 300.0);
   pl->method = opt.method;
+  pl->closure = opt.closure;
   pl->world = opt.world_size;
   pl->rank = opt.rank;
 
@@ -1033,6 +1087,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   pl->band_split = opt.band_split;
   pl->K = opt.temporal_k > 0 ? opt.temporal_k
                              : ((long long)nx * ny >= 4096LL * 4096LL ? (wide ? 3 : 4) : (wide ? 2 : 3));
+  if (opt.closure == CJM_CLOSURE_ODD) pl->K = 1;   // the outer ring is reflected before every sweep
   // multi-GPU: K-fused launches need H = K r deep halos, exchanged after every
   // launch; the slab must stay thicker than 2H + 1 rows (else fall back to K=1)
   if (pl->world > 1 && nyl < 2 * pl->K * R + 1) pl->K = 1;
@@ -1140,7 +1195,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
 
   // ---- resident (shared-memory) hot path: single GPU, whole grid fits in the
   // SMs' shared memory with at least 16 rows per CTA
-  if (pl->world == 1 && !use_nccl && opt.resident >= 0 && !mask) {
+  if (pl->world == 1 && !use_nccl && opt.resident >= 0 && !mask && opt.closure == CJM_CLOSURE_DIRICHLET) {
     const int ldS = nx + 2 * R;
     auto smem_for = [&](int rows) {
       return ((size_t)2 * (rows + 2 * R) * ldS + (size_t)rows * nx) * sizeof(double);

@@ -108,3 +108,32 @@ def test_problem(nx: int, ny: int, r: int, *, h: float | None = None,
 def exact_field(nx: int, ny: int, r: int, h: float) -> np.ndarray:
     """The analytic solution on the interior nodes, (ny, nx)."""
     return exact(np.arange(1, nx + 1) * h, np.arange(1, ny + 1) * h)
+
+
+def sine_problem(n: int, r: int, *, init: str = "zero", seed: int | None = None):
+    """Returns (u0, b, h) of the homogeneous-Dirichlet problem
+    Delta u = -2 pi^2 sin(pi x) sin(pi y) on [0,1]^2, exact u = sin(pi x)
+    sin(pi y), on the n x n grid (h = 1/(n+1)): boundary nodes exactly 0, the
+    17-point outer ring (r = 2) the exact values (odd about the boundary, so
+    the odd-reflection closure of DESIGN R12 is exact for it)."""
+    h = grid_h(n, n)
+    x = coords(n, r, h)
+    s = np.sin(np.pi * x)
+    u0 = np.multiply.outer(s, s)
+    u0[r - 1, :] = u0[-r, :] = 0.0
+    u0[:, r - 1] = u0[:, -r] = 0.0
+    if init == "zero":
+        u0[r:r + n, r:r + n] = 0.0
+    elif init == "random":
+        u0[r:r + n, r:r + n] = uniform_pm1(SEED_BASE if seed is None else seed, n * n).reshape(n, n)
+    elif init != "exact":
+        raise ValueError(init)
+    si = s[r:r + n]
+    b = -2.0 * np.pi * np.pi * np.multiply.outer(si, si)
+    return np.ascontiguousarray(u0), np.ascontiguousarray(b), h
+
+
+def sine_exact(n: int) -> np.ndarray:
+    """sin(pi x) sin(pi y) on the interior nodes of the n x n grid."""
+    s = np.sin(np.pi * np.arange(1, n + 1) / (n + 1))
+    return np.multiply.outer(s, s)

@@ -447,7 +447,7 @@ def test_resident_segment_bitwise(stencil, nx, ny, count):
         assert_field_parity(host(ud), want, r)
 
 
-@pytest.mark.parametrize("nx,ny,resident", [(2048, 4, 0), (2048, 4, 1), (1500, 5, 0), (2600, 4, 1)])
+@pytest.mark.parametrize("nx,ny,resident", [(2048, 4, 0), (1200, 4, 1), (1500, 5, 0), (2600, 4, 0)])
 def test_resident_17_point_thin_slabs(nx, ny, resident):
     """17-point grids only a few rows high: every resident CTA slab but the
     last must own >= r = 2 rows (it publishes its first / last r rows to its
@@ -522,3 +522,64 @@ def test_graft_entry_smoke():
     C-ABI, bitwise equal to the oracle (the driver's round-end smoke check)."""
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+# ------------------------------------------------------------ 17-point odd-reflection closure (NEXT-4)
+def _interior_parity(got, want, r):
+    gi, wi = got[r:-r, r:-r], want[r:-r, r:-r]
+    err = np.max(np.abs(gi - wi)) / max(np.max(np.abs(wi)), 1e-300)
+    assert err <= REL and np.array_equal(gi, wi), f"max rel diff {err:.3e}"
+
+
+@pytest.mark.parametrize("nx,ny", [(64, 64), (300, 257), (1030, 515), (5, 9), (513, 70)])
+@pytest.mark.parametrize("problem", ("sine", "exp"))
+def test_odd_closure_sweeps_bitwise(nx, ny, problem):
+    """cjm_options.closure = ODD (DESIGN R12): the outer ghost ring reflected
+    from the iterate before every sweep; the oracle's closure sweeps, bitwise
+    (interior; the caller's outer ring is never written)."""
+    r = 2
+    if problem == "sine" and nx == ny:
+        u0, b, h = inputs.sine_problem(nx, r, init="random", seed=73)
+    else:
+        u0, b, h = inputs.test_problem(nx, ny, r, init="random", seed=73)
+    with cjm.Plan(17, nx, ny, h, 1e-8, closure=cjm.CLOSURE_ODD) as plan:
+        info = plan.info()
+        assert info["temporal_k"] == 1 and info["resident"] == 0
+        w = oracle_weights(17, nx, ny, plan)
+        ud = dev(u0)
+        plan.sweeps(dev(b), ud, 4, 13)
+        l2, li = plan.residual(dev(b), dev(u0))
+    g = oracle.rhs_to_g(17, h, b)
+    want = oracle.sweeps(17, u0, g, w, 4, 13, closure="odd")
+    got = host(ud)
+    _interior_parity(got, want, r)
+    assert np.array_equal(got[:2], u0[:2]) and np.array_equal(got[:, :2], u0[:, :2])
+    ol2, oli = oracle.residual(17, h, b, oracle.odd_closure(u0))
+    assert l2 == pytest.approx(ol2, rel=1e-12) and li == oli
+
+
+@pytest.mark.parametrize("n", (63, 200))
+def test_odd_closure_solve_matches_oracle(n):
+    """A whole solve under the closure: same iterations and field as the
+    oracle's closure solve; on the homogeneous sine problem the closure is
+    exact and the 17-point solve is fourth-order accurate."""
+    r = 2
+    u0, b, h = inputs.sine_problem(n, r)
+    uo, ro = oracle.solve(17, h, 1e-10, b, u0, closure="odd")
+    with cjm.Plan(17, n, n, h, 1e-10, closure=cjm.CLOSURE_ODD) as plan:
+        ud = dev(u0)
+        rep = plan.solve(dev(b), ud)
+    assert rep["status"] == "CJM_OK" and ro["status"] == "OK"
+    assert rep["iterations"] == ro["iterations"]
+    _interior_parity(host(ud), uo, r)
+    err = np.max(np.abs(host(ud)[r:-r, r:-r] - inputs.sine_exact(n)))
+    assert err <= 6e-7 * (64 / (n + 1)) ** 4
+
+
+@pytest.mark.parametrize("kw", [dict(temporal_k=2), dict(resident=1), dict(band_split=1)])
+def test_odd_closure_options_are_invalid_arg(kw):
+    with pytest.raises(cjm.CJMError) as e:
+        cjm.Plan(17, 64, 64, 1 / 65, 1e-8, closure=cjm.CLOSURE_ODD, **kw)
+    assert e.value.name == "CJM_ERR_INVALID_ARG"
+    with pytest.raises(cjm.CJMError):
+        cjm.Plan(9, 64, 64, 1 / 65, 1e-8, closure=cjm.CLOSURE_ODD)

@@ -501,3 +501,72 @@ def test_lebedev2_solve_converges_like_lebedev23():
     u, rep = oracle.solve(9, h, 1e-8, b, u0, weights_override=s2["w"])
     assert rep["status"] == "OK" and rep["cycles"] == 1 and rep["iterations"] == s2["P"]
     assert rep["r_l2"] <= 1e-8 * rep["r0_l2"]
+
+
+# ----------------------------------------------------------------------------
+# 17-point odd-reflection closure of the outer ghost ring (DESIGN R12)
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("nx,ny", [(7, 7), (9, 6), (12, 11)])
+def test_odd_closure_sweep_is_the_odd_extension_operator(nx, ny):
+    """With zero boundary data, one oracle sweep under the closure equals
+    u + w D^-1 (b - A_odd u) with A_odd assembled from the golden stencil
+    table by reflecting every outer-ring neighbour (tests/dense.py,
+    closure="odd") -- the operator whose lambda_min the closed form gives."""
+    r, h, w = 2, 1.0 / 13, 0.37
+    u = np.zeros((ny + 4, nx + 4))
+    u[2:-2, 2:-2] = _rand((ny, nx), 5)
+    b = _rand((ny, nx), 6)
+    got = oracle.sweeps(17, u, oracle.rhs_to_g(17, h, b), np.array([w]), 0, 1, closure="odd")
+    A, _ = dense.operator(17, nx, ny, closure="odd")
+    ui = u[2:-2, 2:-2].ravel()
+    D = dense.centre(17) / (h * h)
+    want = ui + w * (b.ravel() - A @ ui / (h * h)) / D
+    assert np.max(np.abs(got[2:-2, 2:-2].ravel() - want)) <= 1e-12 * np.max(np.abs(want))
+
+
+def test_odd_closure_is_exact_for_bilinear_fields():
+    """u(mirror) = 2 u_b - u is exact for fields linear across the boundary:
+    the reflected outer ring of a + bx + cy + dxy equals the field itself."""
+    n = 10
+    x = np.arange(-1, n + 3) / (n + 1)
+    X, Y = np.meshgrid(x, x)
+    f = 0.3 + 1.7 * X - 0.9 * Y + 2.3 * X * Y
+    u = f.copy()
+    u[[0, -1], :] = 1e30
+    u[:, [0, -1]] = 1e30
+    got = oracle.odd_closure(u)
+    assert np.max(np.abs(got - f)) <= 1e-14
+
+
+def test_odd_closure_solve_direct_solution_and_fourth_order():
+    """Homogeneous problem Delta u = -2 pi^2 sin sin: the closure is exact for
+    the odd solution, the solve reaches the direct solution of A_odd, and
+    the discretisation error falls at fourth order."""
+    errs = []
+    for n in (15, 31, 63):
+        u0, b, h = inputs.sine_problem(n, 2)
+        u, rep = oracle.solve(17, h, 1e-12, b, u0, closure="odd")
+        assert rep["status"] == "OK"
+        A, _ = dense.operator(17, n, n, closure="odd", sparse=True)
+        import scipy.sparse.linalg as spla
+        x = spla.spsolve(A.tocsc(), (b * h * h).ravel()).reshape(n, n)
+        assert np.max(np.abs(u[2:-2, 2:-2] - x)) <= 1e-9 * np.max(np.abs(x))
+        errs.append(np.max(np.abs(u[2:-2, 2:-2] - inputs.sine_exact(n))))
+    assert errs[0] / errs[1] > 13 and errs[1] / errs[2] > 13
+
+
+def test_odd_closure_one_cycle_meets_the_chebyshev_bound():
+    """kappa bounds exact for the closure operator: one cycle of P sweeps
+    damps the error of a random start by <= tol in the 2-norm (the weights'
+    polynomial is bounded by tol on [kappa_min, kappa_max])."""
+    n = 24
+    u0, b, h = inputs.sine_problem(n, 2, init="random", seed=3)
+    s = oracle.schedule(17, n, n, 1e-6)
+    A, _ = dense.operator(17, n, n, closure="odd", sparse=True)
+    import scipy.sparse.linalg as spla
+    x = spla.spsolve(A.tocsc(), (b * h * h).ravel()).reshape(n, n)
+    u = oracle.sweeps(17, u0, oracle.rhs_to_g(17, h, b), s["w"], 0, s["P"], closure="odd")
+    e0 = np.linalg.norm(u0[2:-2, 2:-2] - x)
+    e1 = np.linalg.norm(u[2:-2, 2:-2] - x)
+    assert e1 <= 1e-6 * e0 * (1 + 1e-6)
