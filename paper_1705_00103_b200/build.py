@@ -38,13 +38,17 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str | None = None) -> str:
-    """Build the library; `defines`/`out` build a measurement variant (e.g.
-    ("CJM_V4_RELEASE=2",)) at another path -- never the product library."""
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str | None = None,
+          src: str | None = None) -> str:
+    """Build the library; `defines` / `out` / `src` (a patched copy of csrc/)
+    build a measurement variant at another path -- never the product library."""
     target = out or LIB
+    if (defines or src) and not out:
+        raise ValueError("measurement builds need their own output path")
     if not force and os.path.exists(target) and \
             os.path.getmtime(target) >= max(os.path.getmtime(d) for d in DEPS):
         return target
+    sources = [os.path.join(src, os.path.basename(f)) for f in SOURCES] if src else SOURCES
     inc, lib = nccl_dirs()
     tmp = target + f".tmp{os.getpid()}"
     objdir = tempfile.mkdtemp(prefix="cjm_build_")
@@ -61,8 +65,8 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
     try:
         # one nvcc per translation unit, in parallel (the sweep-kernel
         # instantiations are spread over kernels_*.cu)
-        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-            results = list(ex.map(compile_one, SOURCES))
+        with ThreadPoolExecutor(max_workers=len(sources)) as ex:
+            results = list(ex.map(compile_one, sources))
         for src, _, r in results:
             if verbose or r.returncode:
                 sys.stderr.write(r.stdout + r.stderr)

@@ -241,6 +241,7 @@ struct cjm_plan_s {
   double* result_host = nullptr;  // pinned, 2 doubles
   cjm::SweepState* state = nullptr;
   unsigned long long* err_bits = nullptr;   // real-error reduction (cjm_solve_ref)
+  unsigned long long* dbg = nullptr;        // CJM_DEBUG_CHECKS: violation count, first code
   void* small_block = nullptr;              // partials | result | state | err_bits
   size_t small_bytes = 0;
   // launch configuration
@@ -407,6 +408,16 @@ cjm_status launch_sweep(cjm_plan_s* pl, int mode, int K, cudaStream_t st, int ro
   }
   sp.chunk_rows = chunk;
   sp.units_static = ustat;
+  sp.buf_elems = (long long)pl->buf_elems;
+#ifdef CJM_DEBUG_CHECKS
+  sp.dbg = pl->dbg;
+  // negative control of the checks: CJM_DEBUG_INJECT=1 understates the buffer
+  // size, so the TMA bounds checks must fire (scripts/sanitize_cases.py --inject)
+  static const bool inject = std::getenv("CJM_DEBUG_INJECT") != nullptr;
+  if (inject) sp.buf_elems /= 2;
+#else
+  sp.dbg = nullptr;
+#endif
   KernelFn k = pick_kernel(pl->stencil, pl->variant, pl->NT, K, mode, pl->nw);
   k<<<grid, block_threads(pl), smem_bytes(pl, K), st>>>(sp);
   CUDA_TRY(cudaGetLastError());
@@ -663,6 +674,24 @@ bool check_layout(const cjm_plan_s* pl, const void* rhs, long long ld_rhs, const
          (pl->stencil != CJM_STENCIL_MASK || pl->mask_ready);   // cjm_mask_set first
 }
 
+// CJM_DEBUG_CHECKS builds: a non-zero device violation count (bounds checks
+// of the sweep kernel, sweep.cuh CheckCode) fails the call.
+cjm_status debug_verify(cjm_plan_s* pl) {
+#ifdef CJM_DEBUG_CHECKS
+  unsigned long long h[2] = {0, 0};
+  CUDA_TRY(cudaMemcpy(h, pl->dbg, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h[0]) {
+    char msg[128];
+    std::snprintf(msg, sizeof(msg), "%llu bounds-check violations, first code %llu", h[0], h[1]);
+    set_error("CJM_DEBUG_CHECKS", msg);
+    return CJM_ERR_CUDA;
+  }
+#else
+  (void)pl;
+#endif
+  return CJM_OK;
+}
+
 double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
@@ -787,6 +816,7 @@ cjm_status solve_impl(cjm_plan_s* pl, const double* rhs, long long ld_rhs, doubl
   rep.kernel_launches = pl->launches;
   rep.status = status;
   if (rep_out) *rep_out = rep;
+  STATUS_TRY(debug_verify(pl));
   return (cjm_status)status;
 }
 
@@ -1266,7 +1296,7 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
                        cudaMemcpyHostToDevice));
   // one small block: partials (2 per CTA), result (2), state, real-error bits
   pl->small_bytes = ((size_t)pl->nctas * 2 + 2) * sizeof(double) + sizeof(cjm::SweepState) +
-                    sizeof(unsigned long long);
+                    3 * sizeof(unsigned long long);
   PLAN_CUDA(cjm::pool_alloc(dev, pl->small_bytes, &pl->small_block));
   pl->partials = static_cast<double*>(pl->small_block);
   if (pl->resident) {
@@ -1276,7 +1306,8 @@ static cjm_status plan_create(cjm_plan_t* out, int stencil, int nx, int ny, doub
   pl->result = pl->partials + (size_t)pl->nctas * 2;
   pl->state = reinterpret_cast<cjm::SweepState*>(pl->result + 2);
   pl->err_bits = reinterpret_cast<unsigned long long*>(pl->state + 1);
-  PLAN_CUDA(cudaMemset(pl->state, 0, sizeof(cjm::SweepState)));
+  pl->dbg = pl->err_bits + 1;
+  PLAN_CUDA(cudaMemset(pl->state, 0, sizeof(cjm::SweepState) + 3 * sizeof(unsigned long long)));
   PLAN_CUDA(cjm::pool_alloc_host(2 * sizeof(double), (void**)&pl->result_host));
   tt.mark("weights+small");
   PLAN_CUDA(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
@@ -1513,7 +1544,7 @@ cjm_status cjm_sweeps(cjm_plan_t p, const double* rhs, long long ld_rhs, double*
   rep.iterations = count;
   rep.kernel_launches = p->launches;
   if (rep_out) *rep_out = rep;
-  return CJM_OK;
+  return debug_verify(p);
 }
 
 cjm_status cjm_residual(cjm_plan_t p, const double* rhs, long long ld_rhs, const double* u,
@@ -1534,7 +1565,7 @@ cjm_status cjm_residual(cjm_plan_t p, const double* rhs, long long ld_rhs, const
   const double sc = std::fabs(p->gscale);
   if (l2) *l2 = std::sqrt(s) / sc;
   if (linf) *linf = m / sc;
-  return CJM_OK;
+  return debug_verify(p);
 }
 
 const char* cjm_status_str(int s) {

@@ -73,6 +73,38 @@ struct SweepParams {
                                // per-CTA ranges, the rest in chunk_rows-unit work items taken
                                // from a device counter (dynamic balancing)
   long long units_static;
+  // bounds of the buffers (CJM_DEBUG_CHECKS builds check every TMA copy, ring
+  // read and store against them and count violations in dbg[0], the first
+  // violation's code in dbg[1]; dbg is NULL in product builds)
+  long long buf_elems;         // doubles per iterate / g buffer
+  unsigned long long* dbg;
+};
+
+// Device-side bounds checks of the CJM_DEBUG_CHECKS build (compute-sanitizer
+// is closed on this GPU pool): a violated condition is counted, never
+// trapped, and the library turns a non-zero count into CJM_ERR_CUDA.
+#ifdef CJM_DEBUG_CHECKS
+#define CJM_CHECK(p, cond, code)                                                  \
+  do {                                                                            \
+    if (!(cond) && (p).dbg) {                                                     \
+      atomicAdd((p).dbg, 1ull);                                                   \
+      atomicCAS((p).dbg + 1, 0ull, (unsigned long long)(code));                   \
+    }                                                                             \
+  } while (0)
+#else
+#define CJM_CHECK(p, cond, code) \
+  do {                           \
+  } while (0)
+#endif
+enum CheckCode {
+  CHK_TMA_U = 1,       // TMA u row source outside the iterate buffer
+  CHK_TMA_G = 2,       // TMA g row source outside the g buffer
+  CHK_TMA_DST = 3,     // TMA destination outside the ring
+  CHK_TMA_ALIGN = 4,   // TMA address / size not 16-byte aligned
+  CHK_STORE = 5,       // store outside the interior of the output buffer
+  CHK_RING_READ = 6,   // consumer ring read outside the ring
+  CHK_TX = 7,          // expected transaction bytes above one stage
+  CHK_DESC = 8         // segment descriptor outside the launch's band
 };
 
 // ---------------------------------------------------------------- PTX helpers

@@ -88,6 +88,9 @@ struct LaneSeg {
   bool in[C], own[C];
   int ja, jb, row_base, uoff;
   double* outp;
+#ifdef CJM_DEBUG_CHECKS
+  const double* out_base;   // the output buffer (bounds checks)
+#endif
 };
 
 // One input row kk (row RI of the ring stage `st`; ring slot ph = kk mod P) of
@@ -117,6 +120,7 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
   // kk - lR), so g needs no register ring.
   {
     const double* row = ucur + RI * TG_::ROW;   // row[2 + j] = column j
+    CJM_CHECK(p, row >= su && row + 2 + C + 2 <= su + (size_t)p.stages * RPS * TG_::ROW, CHK_RING_READ);
     double cc[C];
 #pragma unroll
     for (int j = 0; j < C; j += 2) {
@@ -153,6 +157,7 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
         if (gs < 0) gs += p.stages;
         grow = sg + ((size_t)gs * RPS + GR) * TG_::GROW + ls.uoff;
       }
+      CJM_CHECK(p, grow >= sg && grow + C <= sg + (size_t)p.stages * RPS * TG_::GROW, CHK_RING_READ);
 #pragma unroll
       for (int j = 0; j < C; j += 2) {
         const double2 v = *reinterpret_cast<const double2*>(grow + j);
@@ -196,6 +201,17 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
       }
       push_row<R, K, C>(ws, l + 1, ph, o, l2, l1, r1, r2);
     } else if (active) {
+#ifdef CJM_DEBUG_CHECKS
+      if (STORE) {   // every column this lane may store: interior of a band row
+        const long long off = ls.outp - ls.out_base;
+        const long long orow = off / p.ld, ocol = off - orow * p.ld;
+        for (int j = 0; j < C; ++j)
+          if (FM >= 1 ? (C * lane + j >= E && C * lane + j < WG::WSPAN - E) : ls.own[j])
+            CJM_CHECK(p, off >= 0 && orow >= p.H + p.row0 && orow < p.H + p.row0 + p.nrows &&
+                             ocol + j >= PADL && ocol + j < PADL + p.nx &&
+                             off + j < p.buf_elems, CHK_STORE);
+      }
+#endif
       if (STORE) {
 #pragma unroll
         for (int j = 0; j < C; j += 2) {
@@ -281,6 +297,9 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
   ls.row_base = ja - K * R;
   ls.uoff = wbase + C * lane;                        // shared index of column cl - 2
   ls.outp = dst + (long long)(ja + p.H) * p.ld + PADL + cl;
+#ifdef CJM_DEBUG_CHECKS
+  ls.out_base = dst;
+#endif
   const int nin = jb - ja + 2 * K * R;
   const int nst = (nin + RPS - 1) / RPS;             // ring stages of the segment
   if (c0 + wbase >= p.nx + R) {
@@ -455,6 +474,8 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
           tx = 0;
 #endif
           if (k0 == 0) seg_desc[stage] = make_int4(strip, ja, jb, 1);   // released by the arrive
+          CJM_CHECK(p, tx <= (uint32_t)(RPS * (TG_::ROW + TG_::GROW) * 8), CHK_TX);
+          CJM_CHECK(p, ja >= p.row0 && jb <= p.row0 + p.nrows && ja < jb, CHK_DESC);
           mbar_arrive_expect_tx(&full[stage], tx);
 #pragma unroll
           for (int r = 0; r < RPS; ++r) {
@@ -465,6 +486,26 @@ __global__ void __maxnreg__((V4Regs<STENCIL, K, C>::value)) cjm_sweep_kernel_v4(
             const bool hasg = k < nin && k >= 2 * R && g1 >= p.row_lo && g1 < p.row_hi && gbytes;
 #ifdef CJM_DIAG_NOTMA
             continue;
+#endif
+#ifdef CJM_DEBUG_CHECKS
+            if (hasu) {
+              const long long so = (long long)(gin + p.H) * ld + (PADL - 2) + c0;
+              const long long dso = ((long long)stage * RPS + r) * TG_::ROW;
+              CJM_CHECK(p, so >= 0 && so + ubytes / 8 <= p.buf_elems &&
+                               (PADL - 2) + c0 + (long long)(ubytes / 8) <= ld, CHK_TMA_U);
+              CJM_CHECK(p, dso >= 0 && dso + ubytes / 8 <= (long long)p.stages * RPS * TG_::ROW,
+                        CHK_TMA_DST);
+              CJM_CHECK(p, (so % 2) == 0 && (ubytes % 16) == 0, CHK_TMA_ALIGN);
+            }
+            if (hasg) {
+              const long long so = (long long)(g1 + p.H) * ld + PADL + gc0;
+              const long long dso = ((long long)stage * RPS + r) * TG_::GROW + (gc0 - c0);
+              CJM_CHECK(p, so >= 0 && so + gbytes / 8 <= p.buf_elems && PADL + gc0 + gbytes / 8 <= ld,
+                        CHK_TMA_G);
+              CJM_CHECK(p, dso >= 0 && dso + gbytes / 8 <= (long long)p.stages * RPS * TG_::GROW,
+                        CHK_TMA_DST);
+              CJM_CHECK(p, (so % 2) == 0 && (dso % 2) == 0 && (gbytes % 16) == 0, CHK_TMA_ALIGN);
+            }
 #endif
             if (hasu)
               tma_row_load(su + ((size_t)stage * RPS + r) * TG_::ROW,

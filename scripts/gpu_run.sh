@@ -61,6 +61,18 @@ for T in ${TASKS:-build tests}; do
       timeout 2400 compute-sanitizer --tool ${SANTOOL:-memcheck} --error-exitcode 9 \
         python scripts/sanitize_cases.py > gpurun_out/sanitize_${SANTOOL:-memcheck}_${TAG}.log 2>&1
       echo sanitize_exit=$?; tail -4 gpurun_out/sanitize_${SANTOOL:-memcheck}_${TAG}.log ;;
+    checked)
+      # compute-sanitizer is closed on this pool: the CJM_DEBUG_CHECKS build
+      # (device-side bounds checks of every TMA copy, ring read and store)
+      # runs the GPU suite and the sanitizer cases; CJM_DEBUG_INJECT=1 is the
+      # negative control that must be detected
+      python -c "from paper_1705_00103_b200 import build as b; b.build(force=True, defines=('CJM_DEBUG_CHECKS',), out='build/libcjm_checked.so')" 2>&1 | tail -2
+      CJM_LIB=build/libcjm_checked.so timeout ${TEST_TIMEOUT:-2400} python -m pytest tests -m gpu -q ${TESTS} \
+        > gpurun_out/pytest_checked_${TAG}.log 2>&1; echo checked_pytest_exit=$?; tail -3 gpurun_out/pytest_checked_${TAG}.log
+      CJM_LIB=build/libcjm_checked.so timeout 600 python scripts/sanitize_cases.py > gpurun_out/checked_cases_${TAG}.log 2>&1
+      echo checked_cases_exit=$?; tail -2 gpurun_out/checked_cases_${TAG}.log
+      CJM_LIB=build/libcjm_checked.so CJM_DEBUG_INJECT=1 timeout 300 python scripts/sanitize_cases.py --inject \
+        >> gpurun_out/checked_cases_${TAG}.log 2>&1; echo checked_inject_exit=$?; tail -1 gpurun_out/checked_cases_${TAG}.log ;;
     notma)
       python -c "from paper_1705_00103_b200 import build as b; b.build(force=True, defines=('CJM_DIAG_NOTMA',), out='build/libcjm_notma.so')" 2>&1 | tail -2
       for L in paper_1705_00103_b200/libcjm.so build/libcjm_notma.so; do

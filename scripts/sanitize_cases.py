@@ -36,7 +36,24 @@ CASES = [
 ]
 
 
+def inject():
+    """Negative control (CJM_DEBUG_CHECKS build with CJM_DEBUG_INJECT=1): the
+    library understates the buffer size to the kernel, so its TMA bounds
+    checks must fire and the call must fail."""
+    u0, b, h = inputs.test_problem(300, 200, 1, init="random", seed=71)
+    with cjm.Plan(9, 300, 200, h, 1e-8, resident=-1) as plan:
+        try:
+            plan.sweeps(torch.from_numpy(b).cuda(), torch.from_numpy(u0).cuda(), 0, 8)
+        except cjm.CJMError as e:
+            print("injected violation detected:", e)
+            sys.exit(0)
+    print("injected violation NOT detected")
+    sys.exit(1)
+
+
 def main():
+    if "--inject" in sys.argv:
+        inject()
     bad = 0
     for st, nx, ny, kw, cnt in CASES:
         r = oracle.reach(st)
