@@ -18,7 +18,7 @@ from bench import CONFIGS, make_problem  # noqa: E402
 from paper_1705_00103_b200 import cjm  # noqa: E402
 
 
-def run(config, count, warm, **kw):
+def run(config, count, warm, digest=False, **kw):
     st, nx, ny, tol = CONFIGS[config][:4]
     u0, b, h = make_problem(st, nx, ny, 0, ny)
     ud, bd = torch.from_numpy(u0).cuda(), torch.from_numpy(b).cuda()
@@ -26,12 +26,19 @@ def run(config, count, warm, **kw):
         if warm:
             plan.sweeps(bd, ud, 1, warm)
         rep = plan.sweeps(bd, ud, 1, count)
+        sha = None
+        if digest:   # field after warm + count sweeps (bitwise A/B of builds / launch shapes)
+            import hashlib
+            sha = hashlib.sha256(ud.cpu().numpy().tobytes()).hexdigest()[:16]
     us = 1e6 * rep["sweep_s"] / count
     K = rep["temporal_k"]
     kw = dict(kw, variant=rep["variant"], warps=rep["warps"], stages=rep["stages"], ctas=rep["ctas"],
               temporal_k=K)
-    return dict(config=config, **kw, us_per_sweep=us, glups=nx * ny / (us * 1e-6) / 1e9,
-                gbs_per_launch=24.0 * nx * ny / (K * us * 1e-6) / 1e9)
+    out = dict(config=config, **kw, us_per_sweep=us, glups=nx * ny / (us * 1e-6) / 1e9,
+               gbs_per_launch=24.0 * nx * ny / (K * us * 1e-6) / 1e9, lib=os.environ.get("CJM_LIB", ""))
+    if digest:
+        out["sha"] = sha
+    return out
 
 
 if __name__ == "__main__":
@@ -43,6 +50,7 @@ if __name__ == "__main__":
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--digest", action="store_true")
     ap.add_argument("--temporal-k", type=int, default=0)
     ap.add_argument("--ks", type=lambda v: [int(x) for x in v.split(",")], default=[1, 2, 3, 4])
     ap.add_argument("--variants", type=lambda v: [int(x) for x in v.split(",")], default=[3, 7])
@@ -68,6 +76,6 @@ if __name__ == "__main__":
                     print(json.dumps(dict(config=cfgname, variant=var, tile_w=tw, stages=stg,
                                           ctas_per_sm=cps, temporal_k=K, error=str(e))), flush=True)
     else:
-        print(json.dumps(run(a.config, a.count, a.warm, tile_w=a.tile_w, stages=a.stages,
+        print(json.dumps(run(a.config, a.count, a.warm, digest=a.digest, tile_w=a.tile_w, stages=a.stages,
                              ctas_per_sm=a.ctas_per_sm, temporal_k=a.temporal_k, variant=a.variant,
                              warps=a.warps, chunk_rows=a.chunk_rows, resident=a.resident)))
