@@ -166,7 +166,9 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
       }
     }
     const int G = ls.row_base + kk - (l + 1) * R;           // global row of the output
-    const bool rowin = G >= p.row_lo && G < p.row_hi;
+    // one predicate per node, evaluated without short-circuit branches (the
+    // nested form compiled to three FSEL pairs per node)
+    const bool rowin = (G >= p.row_lo) & (G < p.row_hi);
     double o[C], dd[C];
 #pragma unroll
     for (int j = 0; j < C; ++j) {
@@ -180,8 +182,8 @@ __device__ __forceinline__ void warp_row(WarpState<Point<STENCIL>::R, K, C>& ws,
       }
       const double J = Point<STENCIL>::jacobi_target(uw, x1, x2, g[j]);
       dd[j] = __dsub_rn(J, uw[R]);
-      o[j] = (FM == 2 || ((FM == 1 || ls.in[j]) && rowin)) ? __fma_rn(ws.wl[l], dd[j], uw[R])
-                                                            : uw[R];
+      const bool upd = FM == 2 || (FM == 1 ? rowin : (ls.in[j] & rowin));
+      o[j] = upd ? __fma_rn(ws.wl[l], dd[j], uw[R]) : uw[R];
     }
     const bool active = STEADY || kk >= 2 * (l + 1) * R;   // STEADY: past every warm-up
     if (REDUCE && l == 0 && active && (unsigned)(G - ls.ja) < (unsigned)(ls.jb - ls.ja)) {
@@ -320,6 +322,11 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
   int s0 = 0;
   // full periods, no guards: first those holding a level's warm-up rows
   // (input rows < 2 K r), then the steady ones (every level active)
+#define CJM_V4_STAGE_FM(u, FMX)                                                             \
+  if (u < U)                                                                                \
+    warp_stage<STENCIL, NW, K, C, RPS, ((u < U ? u : 0) * RPS) % P, false, REDUCE, STORE,     \
+               (FM == 1 ? FMX : FM), true>(ws, ls, p, su, sg, s0 + u, (s0 + u) * RPS, nin,   \
+                                           lane, acc_s, acc_m);
 #define CJM_V4_STAGE(u, STEADY)                                                             \
   if (u < U)                                                                                \
     warp_stage<STENCIL, NW, K, C, RPS, ((u < U ? u : 0) * RPS) % P, false, REDUCE, STORE, FM, \
@@ -329,10 +336,23 @@ __device__ __forceinline__ void warp_segment(WarpState<Point<STENCIL>::R, K, C>&
     CJM_V4_STAGE(4, false)
   }
   for (; (s0 + U) * RPS <= nin; s0 += U) {
+    if (FM == 1) {
+      // a segment that touches ghost rows (FM 1: one row test per level)
+      // needs the test only near them: periods whose output rows at every
+      // level (row_base + kk - (l+1) r) are interior run without it
+      const int glo = ls.row_base + s0 * RPS - K * R;
+      const int ghi = ls.row_base + (s0 + U) * RPS - 1 - R;
+      if (glo >= p.row_lo && ghi < p.row_hi) {
+        CJM_V4_STAGE_FM(0, 2) CJM_V4_STAGE_FM(1, 2) CJM_V4_STAGE_FM(2, 2) CJM_V4_STAGE_FM(3, 2)
+        CJM_V4_STAGE_FM(4, 2)
+        continue;
+      }
+    }
     CJM_V4_STAGE(0, true) CJM_V4_STAGE(1, true) CJM_V4_STAGE(2, true) CJM_V4_STAGE(3, true)
     CJM_V4_STAGE(4, true)
   }
 #undef CJM_V4_STAGE
+#undef CJM_V4_STAGE_FM
   static_assert(U <= 5, "stages per period <= 5");
   // tail: fewer than UR rows left, in at most U stages (rows >= nin guarded)
 #define CJM_V4_TAIL(u)                                                                     \
