@@ -23,6 +23,13 @@ DEPS = SOURCES + [os.path.join(CSRC, f) for f in (
     "internal.h")] + [os.path.join(ROOT, "include", "cjm.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+PTXAS_OPT = "-O3"
+# ptxas -O1 for the warp-tiled sweep kernels: its less aggressive scheduling
+# keeps the rotating register rings in place (steady 9-point period 14.5 vs
+# 16.4 instructions per update, 3x fewer register moves, no spills; 17-point
+# 245 registers, no spills) and measured 22.1 vs 22.8 us per sweep at 4096^2,
+# 278 vs 280 at 16384^2, equal for the 17-point (profiles/r02_kernel_ab.jsonl)
+PTXAS_PER_SOURCE = {"kernels_v4_5.cu": "-O1", "kernels_v4_9.cu": "-O1", "kernels_v4_17.cu": "-O1"}
 
 
 def nccl_dirs() -> tuple[str, str]:
@@ -39,11 +46,11 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str | None = None,
-          src: str | None = None) -> str:
+          src: str | None = None, ptxas: str = PTXAS_OPT) -> str:
     """Build the library; `defines` / `out` / `src` (a patched copy of csrc/)
     build a measurement variant at another path -- never the product library."""
     target = out or LIB
-    if (defines or src) and not out:
+    if (defines or src or ptxas != PTXAS_OPT) and not out:
         raise ValueError("measurement builds need their own output path")
     if not force and os.path.exists(target) and \
             os.path.getmtime(target) >= max(os.path.getmtime(d) for d in DEPS):
@@ -54,12 +61,14 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
     objdir = tempfile.mkdtemp(prefix="cjm_build_")
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-ffp-contract=off", "-fmad=false",
-              "-Xptxas", "-v" if verbose else "-O3",
+              "-Xptxas", "__PTXAS__",
               "-I", os.path.join(ROOT, "include"), "-I", inc, *[f"-D{d}" for d in defines]]
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        r = subprocess.run([*common, "-c", src, "-o", obj], capture_output=True, text=True)
+        opt = PTXAS_PER_SOURCE.get(os.path.basename(src), ptxas) if ptxas == PTXAS_OPT else ptxas
+        cmd = [opt + (",-v" if verbose else "") if c == "__PTXAS__" else c for c in common]
+        r = subprocess.run([*cmd, "-c", src, "-o", obj], capture_output=True, text=True)
         return src, obj, r
 
     try:
