@@ -26,7 +26,7 @@
 #include <string>
 #include <utility>
 
-#include "../../include/cjm.h"
+#include "cjm.h"   // include/ (-I)
 #include "internal.h"
 #include "kernels.h"
 #include "resident.cuh"
