@@ -96,3 +96,22 @@ def test_mask_bounds_n_match_dense_eigenvalues(m, nx, ny, kind):
     assert kmax == pytest.approx(hi, rel=1e-6)
     assert kmin == pytest.approx(lo, rel=1e-3)
     assert kmin >= lo * (1 - 1e-9) and kmax <= hi * (1 + 1e-9)   # from inside the spectrum
+
+
+def test_mask_bounds_n_rejects_mismatched_planes():
+    """Every present plane must have the centre plane's shape (the C power
+    iteration would read past a smaller host buffer), and the centre plane
+    is required."""
+    import numpy as np
+    n = 8
+    planes = [None] * 9
+    planes[4] = np.full((n, n), -20.0 / 6.0)
+    for q in (1, 3, 5, 7):
+        planes[q] = np.full((n, n), 4.0 / 6.0)
+    planes[1] = np.full((n - 1, n), 4.0 / 6.0)
+    with pytest.raises(ValueError):
+        cjm.cjm_mask_bounds_n(planes)
+    planes[1] = np.full((n, n), 4.0 / 6.0)
+    planes[4] = None
+    with pytest.raises(ValueError):
+        cjm.cjm_mask_bounds_n(planes)
