@@ -53,7 +53,7 @@ for T in ${TASKS:-build tests}; do
     ncu)
       SW="python scripts/sweep_runner.py --config ${CONFIG:-cjm9_4096} --count 40 ${SWARGS}"
       timeout 300 $SW > gpurun_out/plain_sw_${TAG}.log 2>&1 && \
-      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cjm_sweep_kernel -s 6 -c 2 \
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cjm_sweep_kernel -s 6 -c ${NCU_COUNT:-1} \
         -o gpurun_out/prof_${TAG} -f $SW > gpurun_out/ncu_full_${TAG}.log 2>&1
       echo ncu_full_exit=$?; tail -2 gpurun_out/ncu_full_${TAG}.log ;;
     sanitize)
