@@ -190,6 +190,17 @@ def make_problem(stencil, nx, ny, y0, nyl):
     return np.ascontiguousarray(u0), np.ascontiguousarray(b), h
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 class OracleSample:
     """The oracle as it stands on a bounded segment of the same solve
     (full-size grid, the first sweeps of the schedule), all host cores.  The
@@ -228,6 +239,7 @@ class OracleSample:
 
     def describe(self, dt, glups, iters):
         d = dict(value=glups, unit="GLUPS", cores=self.oracle.num_threads(), kind="oracle",
+                 cpu_model=cpu_model(),
                  sample=f"{self.k} sweeps of the {self.stencil}-point {self.nx}x{self.ny} solve "
                         f"(schedule positions 0..{self.k - 1}), {dt:.1f} s, OpenMP over rows")
         if iters:
