@@ -542,6 +542,13 @@ cjm_status run_resident(cjm_plan_s* pl, long long count, cudaStream_t st) {
   rp.rows = pl->ny_local;
   rp.count = (int)count;
   rp.rows_per_cta = pl->res_rows;
+  rp.buf_elems = (long long)pl->buf_elems;
+  rp.halo_elems = (long long)(pl->res_halo_bytes / sizeof(double));
+#ifdef CJM_DEBUG_CHECKS
+  rp.dbg = pl->dbg;
+#else
+  rp.dbg = nullptr;
+#endif
   CUDA_TRY(cudaMemsetAsync(pl->res_flags, 0, (size_t)pl->res_ctas * sizeof(unsigned int), st));
   void* args[] = {&rp};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pick_resident(pl->stencil), dim3(pl->res_ctas),

@@ -34,6 +34,9 @@ struct ResidentParams {
   int nx, rows;                 // interior columns / rows
   int count;                    // sweeps of this launch
   int rows_per_cta;             // slab height (the last CTA may have fewer)
+  long long buf_elems;          // doubles per iterate / g buffer (CJM_DEBUG_CHECKS)
+  long long halo_elems;         // doubles of the halo area (CJM_DEBUG_CHECKS)
+  unsigned long long* dbg;      // violation counter, first code (NULL in product builds)
 };
 
 __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
@@ -68,12 +71,14 @@ __global__ void __launch_bounds__(512, 1) cjm_resident_kernel(const ResidentPara
   // shared buffers, and my rows of g
   for (int e = tid; e < srows * ldS; e += nt) {
     const int q = e / ldS, c = e - q * ldS;    // local row q <-> interior row r0 - R + q
+    CJM_CHECK(p, (long long)(r0 + q) * p.ld + (PADL - R) + c < p.buf_elems, CHK_TMA_U);
     const double v = src[(long long)(r0 + q) * p.ld + (PADL - R) + c];
     sbuf[0][e] = v;
     sbuf[1][e] = v;
   }
   for (int e = tid; e < nr * p.nx; e += nt) {
     const int q = e / p.nx, c = e - q * p.nx;
+    CJM_CHECK(p, (long long)(r0 + q + R) * p.ld + PADL + c < p.buf_elems, CHK_TMA_G);
     sg[e] = p.g[(long long)(r0 + q + R) * p.ld + PADL + c];   // g rows sit at offset H = R
   }
   __syncthreads();
@@ -105,6 +110,7 @@ __global__ void __launch_bounds__(512, 1) cjm_resident_kernel(const ResidentPara
     if (k + 1 == p.count) { sc ^= 1; break; }
     // ---- publish my boundary rows, then take the neighbours'
     double* hb = my_halo + (size_t)(k & 1) * 2 * R * ldh;
+    CJM_CHECK(p, hb + (size_t)(2 * R - 1) * ldh + p.nx <= p.halo + p.halo_elems, CHK_STORE);
     for (int e = tid; e < R * p.nx; e += nt) {
       const int q = e / p.nx, i = e - q * p.nx;
       hb[(size_t)q * ldh + i] = b[(q + R) * ldS + i + R];                     // first rows
@@ -139,6 +145,7 @@ __global__ void __launch_bounds__(512, 1) cjm_resident_kernel(const ResidentPara
   const double* fin = sbuf[sc];
   for (int e = tid; e < nr * p.nx; e += nt) {
     const int q = e / p.nx, i = e - q * p.nx;
+    CJM_CHECK(p, r0 + q < p.rows && (long long)(r0 + q + R) * p.ld + PADL + i < p.buf_elems, CHK_STORE);
     dst[(long long)(r0 + q + R) * p.ld + PADL + i] = fin[(q + R) * ldS + i + R];
   }
   // ---- advance the device-side state (the whole grid is one launch: use
