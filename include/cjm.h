@@ -149,15 +149,16 @@ typedef struct {
                               levels (the 17-point at temporal_k 4, or tile_w given) */
     int tile_w;            /* variant 3 only: tile columns per CTA, 256 or 512 */
     int ctas_per_sm;       /* resident CTAs per SM of the persistent sweep grid */
-    int stages;            /* depth of the TMA ring (stages of 1 or 2r+1 rows) */
+    int stages;            /* depth of the TMA ring (stages of 2r+1 rows for variant 7,
+                              one row for variant 3) */
     int graph_chunk;       /* sweeps captured per CUDA graph */
     int resident;          /* hot sweeps of grids that fit in the SMs' shared memory run
                               as ONE cooperative launch per cycle with the grid resident
                               in shared memory: 0 = auto (default), 1 = required,
                               -1 = never.  Single GPU only. */
-    int band_split;        /* 1: run every K=1 hot sweep as boundary-band launches +
-                              interior launch (the multi-GPU overlap schedule) even
-                              without NCCL; for tests */
+    int band_split;        /* 1: run every hot launch as two boundary-band launches
+                              (H rows each) + the interior launch (the multi-GPU
+                              overlap schedule) even without NCCL; for tests */
     int warps;             /* variant 7 only: consumer warps per CTA, 4, 5 or 7, or 11
                               (5/9-point at temporal_k 4: one CTA per SM); 0 = the
                               count that keeps the most consumer warps resident per
