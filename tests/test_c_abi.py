@@ -21,9 +21,10 @@ SRC = os.path.join(ROOT, "tests", "c_abi_demo.c")
 @pytest.fixture(scope="module")
 def demo(tmp_path_factory):
     exe = str(tmp_path_factory.mktemp("cabi") / "c_abi_demo")
-    libdir = os.path.dirname(cjm.LIB_PATH)
+    libdir = os.path.dirname(os.path.abspath(cjm.LIB_PATH))   # CJM_LIB may name a measurement build
     subprocess.check_call(["gcc", "-std=c11", "-O2", "-Wall", "-Werror", SRC, "-I",
-                           os.path.join(ROOT, "include"), "-L", libdir, "-l:libcjm.so",
+                           os.path.join(ROOT, "include"), "-L", libdir,
+                           "-l:" + os.path.basename(cjm.LIB_PATH),
                            f"-Wl,-rpath,{libdir}", "-lm", "-o", exe])
     return exe
 
