@@ -219,16 +219,24 @@ class OracleSample:
         self.k = None
 
     def calibrate(self, budget_s):
-        """Sweeps per call so that one call lasts ~budget_s (doubling to 0.5 s)."""
+        """Sweeps per call so that one call lasts ~budget_s.  The per-sweep
+        cost is the marginal one (two calls of c and 3c sweeps, c doubled until
+        the longer call lasts >= 0.5 s): each oracle call also pays a fixed
+        cost (a second full-size buffer), which a long call amortises."""
         c = 1
         while True:
             t0 = time.perf_counter()
             self.oracle.sweeps(self.stencil, self.u0, self.g, self.s["w"], 0, c)
-            per = (time.perf_counter() - t0) / c
-            if per * c >= 0.5 or c >= 4096:
+            t1 = time.perf_counter()
+            self.oracle.sweeps(self.stencil, self.u0, self.g, self.s["w"], 0, 3 * c)
+            t3 = time.perf_counter() - t1
+            t1 -= t0
+            if t3 >= 0.5 or c >= 4096:
                 break
             c *= 2
-        self.k = max(2, int(budget_s / max(per, 1e-9)))
+        per = max((t3 - t1) / (2 * c), t3 / (3 * c) * 0.25, 1e-9)
+        fixed = max(t1 - per * c, 0.0)
+        self.k = max(2, int((budget_s - fixed) / per))
         return self.k
 
     def run(self):
