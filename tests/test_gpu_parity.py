@@ -365,8 +365,9 @@ def test_solve_matches_stored_oracle_digest(name, temporal_k, resident):  # noqa
 
 @pytest.mark.parametrize("stencil,n,first", [(9, 16384, 41471), (17, 8192, 20001)])
 def test_full_size_segment_bitwise(stencil, n, first):
-    """BASELINE full sizes (the 16384^2 target has no stored full-solve digest:
-    its oracle solve takes hours) in the launch configuration bench.py times
+    """BASELINE full sizes (the 16384^2 target's full solve is also compared
+    through its stored digest, test_solve_matches_stored_oracle_digest) in the
+    launch configuration bench.py times
     (default plan: K fused sweeps, dynamic work items, boundary fast modes):
     a segment of scheduled sweeps from a random iterate, whole field bitwise
     equal to the oracle's."""
