@@ -361,7 +361,7 @@ def main():
 
     for k in range(args.warmup):
         rep0 = step()
-        if k == 0:
+        if k == 0 and world > 1:
             # one line per rank (stderr): the NCCL communicator the plan runs on
             print(json.dumps({"rank": rank, "world_size": world, "comm_nranks": rep0["comm_nranks"],
                               "comm_rank": rep0["comm_rank"], "slab": [y0, nyl],
