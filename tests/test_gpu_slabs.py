@@ -149,3 +149,46 @@ def test_external_halo_sweeps_limited_to_one_launch():
         with pytest.raises(cjm.CJMError) as e:
             plan.sweeps(bd, ud, 0, 3)
         assert e.value.name == "CJM_ERR_INVALID_ARG"
+
+
+def test_target_grid_in_8_slabs_deep_halos_bitwise():
+    """The 8-GPU strong-scaling layout of the north_star target on one GPU:
+    16384^2 in 8 row slabs of 2048 rows, K = 4 fused sweeps per launch with
+    H = 4 deep halos and the band-split overlap schedule (external_halo plans,
+    halos moved with device copies after every launch), two launches: bitwise
+    equal to the whole-domain default plan."""
+    n, world, K, launches = 16384, 8, 4, 2
+    free = torch.cuda.mem_get_info()[0]
+    assert free > 40e9, "a B200 holds the whole grid plus the slabs"
+    u0, b, h = inputs.test_problem(n, n, 1, init="random", seed=83)
+    plans = [cjm.Plan(9, n, n, h, 1e-8, world_size=world, rank=g, external_halo=1, temporal_k=K,
+                      band_split=1) for g in range(world)]
+    H = plans[0].ghost_rows
+    assert H == K and plans[0].info()["temporal_k"] == K
+    u_pad = np.pad(u0, ((H - 1, H - 1), (0, 0)))
+    b_pad = np.pad(b, ((H, H), (0, 0)))
+    us, bs, msgs = [], [], []
+    for g in range(world):
+        y0, nyl = cjm.cjm_slab(n, world, g)
+        us.append(torch.from_numpy(u_pad[y0:y0 + nyl + 2 * H].copy()).cuda())
+        bs.append(torch.from_numpy(b_pad[y0:y0 + nyl + 2 * H].copy()).cuda())
+        msgs.append(cjm.cjm_halo_plan(n, H, world, g))
+    for k in range(launches):
+        for g in range(world):
+            plans[g].sweeps(bs[g], us[g], k * K, K)
+        staged = []
+        for g in range(world):
+            for m in msgs[g]:
+                staged.append((m["peer"], g, us[g][m["send_row"]:m["send_row"] + m["rows"]].clone()))
+        for peer, src, blk in staged:
+            m = [x for x in msgs[peer] if x["peer"] == src][0]
+            us[peer][m["recv_row"]:m["recv_row"] + m["rows"]] = blk
+    field = torch.cat([us[g][H:-H] for g in range(world)]).cpu().numpy()
+    for p_ in plans:
+        p_.close()
+    del us, bs
+    with cjm.Plan(9, n, n, h, 1e-8) as whole:
+        ud = torch.from_numpy(u0).cuda()
+        whole.sweeps(torch.from_numpy(b).cuda(), ud, 0, launches * K)
+        ref = ud.cpu().numpy()
+    assert np.array_equal(field, ref[1:-1])
